@@ -1,0 +1,701 @@
+// bnb_host.cpp -- host orchestration above the device engine and the C-ABI.
+//
+// The BnB loop keeps the reference's semantics (bnb_engine.hpp:116-291): a
+// single orchestration thread owns the best-bound queue, the pending leaves
+// and the incumbent; each pass ships one batch to the device, where the
+// relaxation, rounding and branch selection run without per-node host
+// synchronisation; re-optimisation of all candidate supports of the pass runs
+// as one device batch.  Only the queue bookkeeping and child construction
+// (node_model.hpp:77-105) stay on the host.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <map>
+#include <memory>
+#include <queue>
+#include <string>
+#include <vector>
+
+#include "../../include/bnbg.h"
+#include "engine.hpp"
+#include "rng.hpp"
+
+struct bnbg_handle {
+  bnbg::Engine eng;
+};
+
+struct bnbg_pool {
+  struct Rec {
+    std::vector<int> seq;
+    std::vector<double> coef;
+    double objective;
+  };
+  std::vector<Rec> recs;
+};
+
+static thread_local std::string g_last_error;
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+constexpr double kInf = std::numeric_limits<double>::infinity();
+
+int set_err(bnbg_handle* h, int code, const std::string& msg) {
+  g_last_error = msg;
+  if (h) h->eng.err = msg;
+  return code;
+}
+
+// ---- node_model.hpp:22-172 ------------------------------------------------
+struct Node {
+  std::vector<int> j0, j1;  // construction order
+  std::vector<double> warm;
+  double lb = -kInf;
+  int depth = 0;
+  bool is_leaf(int k, int p) const {  // node_model.hpp:33-36
+    return k - (int)j1.size() <= 0 || (int)(j0.size() + j1.size()) >= p;
+  }
+};
+
+void node_states(const Node& nd, int p, std::vector<uint8_t>& st) {  // :40-45
+  st.assign(p, BNBG_FREE);
+  for (int j : nd.j0) st[j] = BNBG_FIXED_ZERO;
+  for (int j : nd.j1) st[j] = BNBG_FIXED_ONE;
+}
+
+void restore_budget(Node& nd, int k, double M, int p, std::vector<uint8_t>& st) {  // :57-68
+  const int kb = k - (int)nd.j1.size();
+  node_states(nd, p, st);
+  double sum = 0.0;
+  for (int j = 0; j < p; ++j)
+    if (st[j] == BNBG_FREE) sum += std::fabs(nd.warm[j]);
+  const double budget = static_cast<double>(kb) * M;
+  if (sum <= budget) return;
+  const double scale = budget / sum * (1.0 - 1e-12);
+  for (int j = 0; j < p; ++j)
+    if (st[j] == BNBG_FREE) nd.warm[j] *= scale;
+}
+
+// node_model.hpp:77-105
+void branch(const Node& nd, int j, const double* beta, int k, double M, int p, Node& c0, Node& c1,
+            std::vector<uint8_t>& st, std::vector<uint8_t>& st2) {
+  node_states(nd, p, st);
+  c0 = nd;
+  c0.j0.push_back(j);
+  c0.warm.assign(beta, beta + p);
+  c0.warm[j] = 0.0;
+  c0.depth = nd.depth + 1;
+  restore_budget(c0, k, M, p, st2);
+  c1 = nd;
+  c1.j1.push_back(j);
+  c1.warm.assign(beta, beta + p);
+  c1.depth = nd.depth + 1;
+  if (k - (int)c1.j1.size() <= 0) {
+    for (int r = 0; r < p; ++r) {
+      if (r != j && st[r] == BNBG_FREE) {
+        c1.j0.push_back(r);
+        c1.warm[r] = 0.0;
+      }
+    }
+  }
+  restore_budget(c1, k, M, p, st2);
+}
+
+// best-bound queue with FIFO tie-break (node_model.hpp:114-148)
+class NodeQueue {
+ public:
+  void push(Node nd) {
+    const double b = nd.lb;
+    heap_.push(Entry{b, seq_++, std::make_shared<Node>(std::move(nd))});
+  }
+  bool empty() const { return heap_.empty(); }
+  double global_lb() const { return heap_.empty() ? kInf : heap_.top().bound; }
+  Node pop() {
+    Entry e = heap_.top();
+    heap_.pop();
+    return std::move(*e.node);
+  }
+
+ private:
+  struct Entry {
+    double bound;
+    uint64_t seq;
+    std::shared_ptr<Node> node;
+    bool operator>(const Entry& o) const {
+      if (bound != o.bound) return bound > o.bound;
+      return seq > o.seq;
+    }
+  };
+  std::priority_queue<Entry, std::vector<Entry>, std::greater<Entry>> heap_;
+  uint64_t seq_ = 0;
+};
+
+// ---- search policies: solve (bnb_engine.hpp:304-307), rashomon (:169-196)
+struct Policy {
+  int kind = 0;
+  double delta = 1e-6;
+  double eps = 0.0;
+  long long cap = -1;
+  struct Staged {
+    std::vector<int> seq;
+    std::vector<double> coef;
+    double objective;
+  };
+  std::vector<Staged> staged;
+  std::map<std::vector<int>, int> staged_index;
+  std::priority_queue<double> best_heap;
+  double best_objective = kInf;
+
+  double nth_best() const {
+    if (cap < 0) return kInf;
+    if ((long long)best_heap.size() < cap) return kInf;
+    return best_heap.top();
+  }
+  double threshold(double ub) const {
+    if (kind == 0) {
+      if (!std::isfinite(ub)) return kInf;
+      return ub - delta * std::max(1.0, std::fabs(ub));
+    }
+    const double tau = std::min(std::isfinite(ub) ? (1.0 + eps) * ub : kInf, nth_best());
+    return std::nextafter(tau, kInf);
+  }
+  void on_model(const int* seq, int len, const double* coef, double objective) {
+    if (kind != 1) return;
+    best_objective = std::min(best_objective, objective);
+    const double tau_now = std::min((1.0 + eps) * best_objective, nth_best()) + 1e-9;
+    if (objective > tau_now) return;
+    std::vector<int> key(seq, seq + len);
+    std::sort(key.begin(), key.end());
+    if (staged_index.count(key)) return;
+    staged_index.emplace(std::move(key), (int)staged.size());
+    staged.push_back({std::vector<int>(seq, seq + len), std::vector<double>(coef, coef + len),
+                      objective});
+    if (cap >= 0) {
+      if ((long long)best_heap.size() < cap)
+        best_heap.push(objective);
+      else if (objective < best_heap.top()) {
+        best_heap.pop();
+        best_heap.push(objective);
+      }
+    }
+  }
+};
+
+struct Timer {
+  double& acc;
+  Clock::time_point t0;
+  explicit Timer(double& a) : acc(a), t0(Clock::now()) {}
+  ~Timer() { acc += std::chrono::duration<double>(Clock::now() - t0).count(); }
+};
+
+int auto_batch(uint64_t budget, int n, int p, int k, int loss) {  // bnb_engine.hpp:75-88
+  if (budget == 0) return -1;
+  const double lb_bytes = 8.0 * 5.0 * p;
+  const double loss_arrays = loss == BNBG_LOGISTIC ? 3.0 : 2.0;
+  const double reopt_bytes = 8.0 * (loss_arrays * n + 2.0 * k);
+  const double capacity = 0.9 * static_cast<double>(budget) / (lb_bytes + reopt_bytes);
+  if (capacity < 2.0) return 1;
+  int size = 1;
+  while (2.0 * size <= capacity && size < (1 << 29)) size <<= 1;
+  return size;
+}
+
+bnbg::RelaxParams relax_params(const bnbg_relax_cfg& c) {
+  bnbg::RelaxParams r;
+  r.max_iterations = c.max_iterations;
+  r.gap_tolerance = c.gap_tolerance;
+  r.check_interval = c.check_interval;
+  r.acceleration = c.acceleration;
+  return r;
+}
+
+// bnb_engine.hpp:116-291 run_bnb
+int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certificate* cert,
+            bnbg_dual_hook on_dual, bnbg_boundary_hook on_boundary, void* user) {
+  bnbg::Engine& eng = h->eng;
+  const int n = eng.n, p = eng.p, k = eng.k;
+  const double M = eng.M;
+  const auto wall_start = Clock::now();
+  auto elapsed = [&]() { return std::chrono::duration<double>(Clock::now() - wall_start).count(); };
+  cert->optimal_value = kInf;
+  cert->support_len = 0;
+  cert->gap_percent = 0.0;
+  cert->lower_bound = -kInf;
+  cert->nodes_processed = cert->lb_batches = cert->reopt_batches = 0;
+  cert->lower_bound_seconds = cert->reoptimization_seconds = cert->transfer_seconds = 0.0;
+  cert->branch_generate_seconds = cert->total_seconds = 0.0;
+  cert->relax_iterations = cert->node_iterations = cert->reopt_supports = 0;
+  cert->device_seconds = 0.0;
+  cert->status = BNBG_STATUS_OPTIMAL;
+  if (cfg.relax.check_interval < 1 || cfg.relax.max_iterations < 1)
+    return set_err(h, BNBG_INPUT_ERROR, "relax config: max_iterations, check_interval >= 1");
+  bnbg::RelaxParams rp = relax_params(cfg.relax);
+  {
+    Timer t(cert->lower_bound_seconds);
+    if (cfg.relax.smoothness > 0.0) eng.L = cfg.relax.smoothness;
+  }
+  const int batch_size =
+      cfg.batch_size > 0 ? cfg.batch_size : auto_batch(cfg.memory_budget, n, p, k, eng.loss);
+  if (batch_size < 1) return set_err(h, BNBG_INPUT_ERROR, "assemble_batch: batch_size >= 1");
+  cert->batch_size_used = batch_size;
+
+  NodeQueue queue;
+  {
+    Node root;  // node_model.hpp:47-52
+    root.warm.assign(p, 0.0);
+    queue.push(std::move(root));
+  }
+  std::vector<Node> pending;
+  double inc_obj = kInf;
+  std::vector<int> inc_sup;
+  std::vector<double> inc_coef;
+  int status = BNBG_STATUS_OPTIMAL;
+  std::vector<uint8_t> st, st2;
+  std::vector<double> warm;
+  bnbg::BatchLists lists;
+  bnbg::PassResult pr;
+
+  while (!queue.empty() || !pending.empty()) {
+    if (elapsed() > cfg.time_limit) {
+      status = BNBG_STATUS_TIME_LIMIT;
+      break;
+    }
+    const double threshold = pol.threshold(inc_obj);
+    std::vector<Node> relax_nodes, leaves;
+    {
+      Timer t(cert->transfer_seconds);
+      int popped = 0, discarded = 0;  // assemble_batch node_model.hpp:158-172
+      std::vector<Node> batch;
+      while (!queue.empty() && popped < batch_size) {
+        Node nd = queue.pop();
+        if (nd.lb >= threshold) {
+          ++discarded;
+          continue;
+        }
+        batch.push_back(std::move(nd));
+        ++popped;
+      }
+      cert->nodes_processed += popped + discarded;
+      for (Node& leaf : pending) {
+        ++cert->nodes_processed;
+        if (leaf.lb >= threshold) continue;
+        leaves.push_back(std::move(leaf));
+      }
+      pending.clear();
+      for (Node& nd : batch) {
+        if (nd.is_leaf(k, p))
+          leaves.push_back(std::move(nd));
+        else
+          relax_nodes.push_back(std::move(nd));
+      }
+      // pack the batch as CSR lists + warm block (the device packer expands it)
+      const int m = (int)relax_nodes.size();
+      lists.m = m;
+      lists.z_off.assign(m + 1, 0);
+      lists.o_off.assign(m + 1, 0);
+      lists.z_idx.clear();
+      lists.o_idx.clear();
+      warm.resize((size_t)p * m);
+      for (int b = 0; b < m; ++b) {
+        const Node& nd = relax_nodes[b];
+        lists.z_idx.insert(lists.z_idx.end(), nd.j0.begin(), nd.j0.end());
+        lists.o_idx.insert(lists.o_idx.end(), nd.j1.begin(), nd.j1.end());
+        lists.z_off[b + 1] = (int)lists.z_idx.size();
+        lists.o_off[b + 1] = (int)lists.o_idx.size();
+        std::memcpy(warm.data() + (size_t)b * p, nd.warm.data(), sizeof(double) * p);
+      }
+    }
+    if (relax_nodes.empty() && leaves.empty()) continue;
+
+    const int m = (int)relax_nodes.size();
+    if (m > 0) {
+      Timer t(cert->lower_bound_seconds);
+      const int rc = eng.relax_lists(lists, warm.data(), rp, threshold, on_dual != nullptr, pr);
+      if (rc) return set_err(h, rc, eng.err);
+      ++cert->lb_batches;
+      cert->relax_iterations += pr.iterations;
+      cert->node_iterations += pr.node_iterations;
+      if (on_dual) {  // replay in the reference's order (relaxation.hpp:201-203)
+        for (int e = 0; e < pr.n_evals; ++e)
+          for (int b = 0; b < m; ++b) {
+            const double psi = pr.trace[(size_t)e * m + b];
+            if (std::isnan(psi)) continue;
+            const Node& nd = relax_nodes[b];
+            on_dual(user, (int)nd.j0.size(), nd.j0.data(), (int)nd.j1.size(), nd.j1.data(), psi);
+          }
+      }
+    }
+
+    // one re-optimization batch: leaf supports, then rounded columns (:193-212)
+    std::vector<int> offsets(1, 0), sidx;
+    {
+      Timer t(cert->reoptimization_seconds);
+      for (const Node& leaf : leaves) {
+        sidx.insert(sidx.end(), leaf.j1.begin(), leaf.j1.end());
+        offsets.push_back((int)sidx.size());
+      }
+      for (int b = 0; b < m; ++b) {
+        if (pr.status[b] == BNBG_PRUNABLE) continue;
+        const int* row = pr.sup.data() + (size_t)b * std::max(k, 1);
+        sidx.insert(sidx.end(), row, row + pr.len[b]);
+        offsets.push_back((int)sidx.size());
+      }
+    }
+    const int nsup = (int)offsets.size() - 1;
+    std::vector<double> coef(sidx.size() + 1), obj(nsup + 1);
+    if (nsup > 0) {
+      Timer t(cert->reoptimization_seconds);
+      const int rc = eng.reoptimize(nsup, offsets.data(), sidx.data(), coef.data(), obj.data());
+      if (rc) return set_err(h, rc, eng.err);
+      ++cert->reopt_batches;
+      cert->reopt_supports += nsup;
+    }
+    {
+      Timer t(cert->branch_generate_seconds);
+      for (int s = 0; s < nsup; ++s) {  // incumbent update (bnb_engine.hpp:216-240)
+        const int len = offsets[s + 1] - offsets[s];
+        const int* sq = sidx.data() + offsets[s];
+        const double* cf = coef.data() + offsets[s];
+        pol.on_model(sq, len, cf, obj[s]);
+        if (obj[s] < inc_obj) {
+          inc_obj = obj[s];
+          std::vector<int> order(len);
+          for (int i = 0; i < len; ++i) order[i] = i;
+          std::sort(order.begin(), order.end(), [&](int a, int b) { return sq[a] < sq[b]; });
+          inc_sup.resize(len);
+          inc_coef.resize(len);
+          for (int i = 0; i < len; ++i) {
+            inc_sup[i] = sq[order[i]];
+            inc_coef[i] = cf[order[i]];
+          }
+        }
+      }
+      const double post_threshold = pol.threshold(inc_obj);
+      for (int b = 0; b < m; ++b) {  // :243-256
+        if (pr.status[b] == BNBG_PRUNABLE) continue;
+        Node& nd = relax_nodes[b];
+        nd.lb = std::max(nd.lb, pr.bounds[b]);
+        if (nd.lb >= post_threshold) continue;
+        const int j = pr.jbranch[b];
+        if (j < 0)
+          return set_err(h, BNBG_LOGIC_ERROR, "select_branch_variable: no free coordinate");
+        Node c0, c1;
+        branch(nd, j, pr.beta.data() + (size_t)b * p, k, M, p, c0, c1, st, st2);
+        for (Node* child : {&c0, &c1}) {
+          if (child->is_leaf(k, p))
+            pending.push_back(std::move(*child));
+          else
+            queue.push(std::move(*child));
+        }
+      }
+    }
+    if (on_boundary) {  // :259-265
+      double lb = queue.global_lb();
+      for (const Node& leaf : pending) lb = std::min(lb, leaf.lb);
+      on_boundary(user, std::min(lb, inc_obj), inc_obj);
+    }
+  }
+
+  const double ub = inc_obj;  // certificate (:268-290)
+  cert->status = status;
+  cert->optimal_value = ub;
+  cert->support_len = (int)inc_sup.size();
+  for (size_t i = 0; i < inc_sup.size(); ++i) {
+    if (cert->support) cert->support[i] = inc_sup[i];
+    if (cert->coefficients) cert->coefficients[i] = inc_coef[i];
+  }
+  if (status == BNBG_STATUS_OPTIMAL) {
+    cert->lower_bound = ub;
+    cert->gap_percent = 0.0;
+  } else {
+    double lb = queue.global_lb();
+    for (const Node& leaf : pending) lb = std::min(lb, leaf.lb);
+    lb = std::min(lb, ub);
+    cert->lower_bound = lb;
+    cert->gap_percent =
+        !std::isfinite(ub) ? 100.0 : 100.0 * (ub - lb) / std::max(std::fabs(ub), 1e-12);
+  }
+  cert->total_seconds = elapsed();
+  return BNBG_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+void bnbg_relax_cfg_default(bnbg_relax_cfg* c) {
+  c->max_iterations = 2000;
+  c->gap_tolerance = 1e-6;
+  c->check_interval = 10;
+  c->acceleration = 1;
+  c->smoothness = 0.0;
+  c->workers = 1;
+}
+
+void bnbg_solver_cfg_default(bnbg_solver_cfg* c) {
+  c->batch_size = 0;
+  c->memory_budget = uint64_t(1) << 30;
+  c->time_limit = kInf;
+  c->prune_slack = 1e-6;
+  bnbg_relax_cfg_default(&c->relax);
+  c->profile = 0;
+  c->workers = 1;
+}
+
+int bnbg_auto_batch_size(uint64_t memory_budget, int n, int p, int k, int loss) {
+  return auto_batch(memory_budget, n, p, k, loss);
+}
+
+int bnbg_validate(const double* X, const double* y, int n, int p, int loss, int k, double M,
+                  double lambda2) {  // problem.hpp:36-51
+  if (n <= 0 || p <= 0) return set_err(nullptr, BNBG_INPUT_ERROR, "instance: empty design matrix");
+  for (size_t i = 0; i < (size_t)n * p; ++i)
+    if (!std::isfinite(X[i])) return set_err(nullptr, BNBG_INPUT_ERROR, "instance: non-finite entries");
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(y[i])) return set_err(nullptr, BNBG_INPUT_ERROR, "instance: non-finite entries");
+  if (k < 1 || k > p) return set_err(nullptr, BNBG_INPUT_ERROR, "instance: k must satisfy 1 <= k <= p");
+  if (!(M > 0.0)) return set_err(nullptr, BNBG_INPUT_ERROR, "instance: M must be positive");
+  if (!(lambda2 > 0.0)) return set_err(nullptr, BNBG_INPUT_ERROR, "instance: lambda2 must be positive");
+  if (loss != BNBG_SQUARED && loss != BNBG_LOGISTIC)
+    return set_err(nullptr, BNBG_INPUT_ERROR, "instance: unknown loss");
+  if (loss == BNBG_LOGISTIC)
+    for (int i = 0; i < n; ++i)
+      if (y[i] != 1.0 && y[i] != -1.0)
+        return set_err(nullptr, BNBG_INPUT_ERROR, "logistic label must be -1 or +1");
+  return BNBG_OK;
+}
+
+// problem.hpp:70-132.  AR(1) Toeplitz Cholesky factor in closed form:
+// L[j][0] = rho^j, L[j][l] = rho^(j-l) sqrt(1-rho^2); row i = L g_i summed in
+// ascending l with fma (bit-identical to the oracle's restatement).
+int bnbg_generate_synthetic(int n, int p, int k, double rho, int loss, double snr, uint64_t seed,
+                            double* X, double* y, int32_t* support) {
+  if (n < 1 || p < 1) return set_err(nullptr, BNBG_INPUT_ERROR, "generator: n, p >= 1");
+  if (k < 1 || k > p) return set_err(nullptr, BNBG_INPUT_ERROR, "generator: k must satisfy 1 <= k <= p");
+  if (rho < 0.0 || rho >= 1.0)
+    return set_err(nullptr, BNBG_INPUT_ERROR, "generator: correlation must lie in [0, 1)");
+  if (!(snr > 0.0)) return set_err(nullptr, BNBG_INPUT_ERROR, "generator: snr must be positive");
+  bnbg::Xoshiro256pp rng(seed);
+  std::vector<double> G((size_t)n * p);
+  for (auto& g : G) g = rng.gaussian();
+  if (rho > 0.0) {
+    std::vector<double> pw(p);
+    pw[0] = 1.0;
+    for (int d = 1; d < p; ++d) pw[d] = pw[d - 1] * rho;
+    const double sr = std::sqrt(1.0 - rho * rho);
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < n; ++i) {
+      const double* g = G.data() + (size_t)i * p;
+      for (int j = 0; j < p; ++j) {
+        double acc = pw[j] * g[0];
+        for (int l = 1; l <= j; ++l) acc = std::fma(pw[j - l] * sr, g[l], acc);
+        X[(size_t)j * n + i] = acc;
+      }
+    }
+  } else {
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < p; ++j) X[(size_t)j * n + i] = G[(size_t)i * p + j];
+  }
+  const int step = p / k;
+  for (int t = 1; t <= k; ++t) support[t - 1] = t * step - 1;
+  std::vector<double> signal(n, 0.0);
+  for (int t = 0; t < k; ++t) {
+    const double* col = X + (size_t)support[t] * n;
+    for (int i = 0; i < n; ++i) signal[i] += col[i];
+  }
+  if (loss == BNBG_SQUARED) {
+    double s2 = 0.0;
+    for (double v : signal) s2 += v * v;
+    const double sigma2 = std::sqrt(s2) / snr;
+    const double sd = std::sqrt(sigma2);
+    for (int i = 0; i < n; ++i) y[i] = signal[i] + sd * rng.gaussian();
+  } else {
+    for (int i = 0; i < n; ++i) {
+      const double t = signal[i];
+      double prob;
+      if (t >= 0.0) {
+        const double e = std::exp(-t);
+        prob = 1.0 / (1.0 + e);
+      } else {
+        const double e = std::exp(t);
+        prob = e / (1.0 + e);
+      }
+      y[i] = rng.uniform() < prob ? 1.0 : -1.0;
+    }
+  }
+  return BNBG_OK;
+}
+
+int bnbg_create(const double* X, const double* y, int n, int p, int loss, int k, double M,
+                double lambda2, double L, int device, bnbg_handle** out) {
+  *out = nullptr;
+  if (int rc = bnbg_validate(X, y, n, p, loss, k, M, lambda2)) return rc;
+  auto* h = new bnbg_handle();
+  const int rc = h->eng.init(X, y, n, p, loss, k, M, lambda2, L, device);
+  if (rc) {
+    g_last_error = h->eng.err;
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return BNBG_OK;
+}
+
+void bnbg_destroy(bnbg_handle* h) { delete h; }
+
+const char* bnbg_last_error(const bnbg_handle* h) {
+  if (h && !h->eng.err.empty()) return h->eng.err.c_str();
+  return g_last_error.c_str();
+}
+
+double bnbg_smoothness(bnbg_handle* h) { return h->eng.L; }
+
+int bnbg_relax_batch(bnbg_handle* h, const bnbg_relax_cfg* cfg, int m, const uint8_t* state,
+                     const int32_t* kbar, const double* warm, double prune_threshold,
+                     double* beta_out, double* bounds_out, int32_t* status_out,
+                     int32_t* iters_out, bnbg_trace_fn trace, void* user) {
+  bnbg_relax_cfg c;
+  if (cfg)
+    c = *cfg;
+  else
+    bnbg_relax_cfg_default(&c);
+  if (m <= 0) return set_err(h, BNBG_INPUT_ERROR, "solve_batch_relaxation: empty batch");
+  if (c.check_interval < 1 || c.max_iterations < 1)
+    return set_err(h, BNBG_INPUT_ERROR, "relax config: max_iterations, check_interval >= 1");
+  const double saved_L = h->eng.L;
+  if (c.smoothness > 0.0) h->eng.L = c.smoothness;
+  bnbg::PassResult pr;
+  const int rc =
+      h->eng.relax_raw(m, relax_params(c), prune_threshold, state, kbar, warm, trace != nullptr, pr);
+  h->eng.L = saved_L;
+  if (rc) return set_err(h, rc, h->eng.err);
+  std::memcpy(beta_out, pr.beta.data(), sizeof(double) * pr.beta.size());
+  std::memcpy(bounds_out, pr.bounds.data(), sizeof(double) * m);
+  std::memcpy(status_out, pr.status.data(), sizeof(int) * m);
+  std::memcpy(iters_out, pr.iters.data(), sizeof(int) * m);
+  if (trace) {
+    for (int e = 0; e < pr.n_evals; ++e)
+      for (int b = 0; b < m; ++b) {
+        const double psi = pr.trace[(size_t)e * m + b];
+        if (!std::isnan(psi)) trace(user, b, psi);
+      }
+  }
+  return BNBG_OK;
+}
+
+int bnbg_round_support(bnbg_handle* h, int m, const double* beta, const uint8_t* state,
+                       const int32_t* kbar, const int32_t* one_off, const int32_t* one_idx,
+                       int32_t* support_out, int32_t* len_out) {
+  const int rc = h->eng.round_select(m, beta, state, kbar, one_off, one_idx, support_out, len_out,
+                                     nullptr);
+  return rc ? set_err(h, rc, h->eng.err) : BNBG_OK;
+}
+
+int bnbg_select_branch(bnbg_handle* h, int m, const double* beta, const uint8_t* state,
+                       int32_t* j_out) {
+  std::vector<int> kb(std::max(m, 1), 0);
+  const int rc =
+      h->eng.round_select(m, beta, state, kb.data(), nullptr, nullptr, nullptr, nullptr, j_out);
+  return rc ? set_err(h, rc, h->eng.err) : BNBG_OK;
+}
+
+int bnbg_reoptimize(bnbg_handle* h, int nsup, const int32_t* offsets, const int32_t* idx,
+                    double* coef_out, double* obj_out) {
+  for (int s = 0; s < nsup; ++s)
+    for (int t = offsets[s]; t < offsets[s + 1]; ++t)
+      if (idx[t] < 0 || idx[t] >= h->eng.p)
+        return set_err(h, BNBG_INPUT_ERROR, "reoptimize_supports: index out of range");
+  const int rc = h->eng.reoptimize(nsup, offsets, idx, coef_out, obj_out);
+  return rc ? set_err(h, rc, h->eng.err) : BNBG_OK;
+}
+
+int bnbg_gemm(bnbg_handle* h, int trans, int m, const double* B, double* C) {
+  const int rc = h->eng.gemm_probe(trans, m, B, C);
+  return rc ? set_err(h, rc, h->eng.err) : BNBG_OK;
+}
+
+int bnbg_solve(bnbg_handle* h, const bnbg_solver_cfg* cfg, bnbg_certificate* cert,
+               bnbg_dual_hook on_dual, bnbg_boundary_hook on_boundary, void* user) {
+  bnbg_solver_cfg c;
+  if (cfg)
+    c = *cfg;
+  else
+    bnbg_solver_cfg_default(&c);
+  Policy pol;
+  pol.kind = 0;
+  pol.delta = c.prune_slack;
+  const double saved_L = h->eng.L;
+  const int rc = run_bnb(h, c, pol, cert, on_dual, on_boundary, user);
+  h->eng.L = saved_L;
+  return rc;
+}
+
+int bnbg_collect_rashomon(bnbg_handle* h, const bnbg_solver_cfg* cfg, double epsilon, long long cap,
+                          bnbg_certificate* cert, bnbg_pool** pool_out) {
+  *pool_out = nullptr;
+  if (epsilon < 0.0) return set_err(h, BNBG_INPUT_ERROR, "rashomon: epsilon must be nonnegative");
+  bnbg_solver_cfg c;
+  if (cfg)
+    c = *cfg;
+  else
+    bnbg_solver_cfg_default(&c);
+  Policy pol;
+  pol.kind = 1;
+  pol.eps = epsilon;
+  pol.cap = cap;
+  const double saved_L = h->eng.L;
+  const int rc = run_bnb(h, c, pol, cert, nullptr, nullptr, nullptr);
+  h->eng.L = saved_L;
+  if (rc) return rc;
+  // compaction against the final threshold (rashomon.hpp:201-216)
+  const double tau_final = (1.0 + epsilon) * cert->optimal_value + 1e-9;
+  std::vector<int> live;
+  for (int i = 0; i < (int)pol.staged.size(); ++i)
+    if (pol.staged[i].objective <= tau_final) live.push_back(i);
+  std::sort(live.begin(), live.end(), [&](int a, int b) {
+    if (pol.staged[a].objective != pol.staged[b].objective)
+      return pol.staged[a].objective < pol.staged[b].objective;
+    return pol.staged[a].seq < pol.staged[b].seq;
+  });
+  if (cap >= 0 && (long long)live.size() > cap) live.resize(cap);
+  auto* pool = new bnbg_pool();
+  for (int i : live)
+    pool->recs.push_back({pol.staged[i].seq, pol.staged[i].coef, pol.staged[i].objective});
+  *pool_out = pool;
+  return BNBG_OK;
+}
+
+int bnbg_pool_size(const bnbg_pool* pool) { return pool ? (int)pool->recs.size() : 0; }
+
+int bnbg_pool_record(const bnbg_pool* pool, int i, int32_t* seq_out, double* coef_out,
+                     double* objective_out) {
+  const auto& r = pool->recs[i];
+  std::memcpy(seq_out, r.seq.data(), sizeof(int) * r.seq.size());
+  std::memcpy(coef_out, r.coef.data(), sizeof(double) * r.coef.size());
+  *objective_out = r.objective;
+  return (int)r.seq.size();
+}
+
+void bnbg_pool_free(bnbg_pool* pool) { delete pool; }
+
+long long bnbg_kernel_launches(const bnbg_handle* h) { return h->eng.launches; }
+
+int bnbg_gemm_stats(const bnbg_handle* h, double* gemm_ms, double* gemm_flops,
+                    long long* gemm_launches) {
+  const auto& e = h->eng;
+  if (gemm_ms) *gemm_ms = e.kc_ms[bnbg::KC_GEMM_NN] + e.kc_ms[bnbg::KC_GEMM_TN];
+  if (gemm_flops) *gemm_flops = e.kc_flops[bnbg::KC_GEMM_NN] + e.kc_flops[bnbg::KC_GEMM_TN];
+  if (gemm_launches)
+    *gemm_launches = e.kc_launches[bnbg::KC_GEMM_NN] + e.kc_launches[bnbg::KC_GEMM_TN];
+  return BNBG_OK;
+}
+
+void bnbg_set_timing(bnbg_handle* h, int enabled) { h->eng.timing = enabled != 0; }
+
+}  // extern "C"

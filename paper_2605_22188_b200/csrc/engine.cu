@@ -1,0 +1,747 @@
+// engine.cu -- device engine: instance upload, GEMM planning, the relaxation
+// loop (relaxation.hpp:163-255), rounding/branch selection and re-opt.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "engine.hpp"
+#include "gemm.cuh"
+#include "node_kernels.cuh"
+#include "rng.hpp"
+
+namespace bnbg {
+
+#define CK(call)                                          \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);   \
+  } while (0)
+
+#define CKL(what)                                         \
+  do {                                                    \
+    ++launches;                                           \
+    cudaError_t e_ = cudaGetLastError();                  \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what);    \
+  } while (0)
+
+static int next_pow2(int v) {
+  int r = 1;
+  while (r < v) r <<= 1;
+  return r;
+}
+
+Engine::~Engine() {
+  cudaFree(dX_);
+  cudaFree(dy_);
+  cudaFree(dB_);
+  cudaFree(dV_);
+  cudaFree(dG_);
+  cudaFree(dR_);
+  cudaFree(dPL_);
+  cudaFree(dPC_);
+  cudaFree(dT_);
+  cudaFree(dBest_);
+  cudaFree(dLast_);
+  cudaFree(dState_);
+  cudaFree(dFrozen_);
+  cudaFree(dKbar_);
+  cudaFree(dPf_);
+  cudaFree(dStatus_);
+  cudaFree(dIters_);
+  cudaFree(dAct_);
+  cudaFree(dMa_);
+  cudaFree(dErr_);
+  cudaFree(dSup_);
+  cudaFree(dLen_);
+  cudaFree(dJb_);
+  cudaFree(dAux_);
+  if (hPin_) cudaFreeHost(hPin_);
+  if (ev0_) cudaEventDestroy(ev0_);
+  if (ev1_) cudaEventDestroy(ev1_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+int Engine::fail(int code, const std::string& msg) {
+  err = msg;
+  return code;
+}
+
+int Engine::cuda_fail(cudaError_t e, const char* what) {
+  err = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+  return 4;  // BNBG_CUDA_ERROR
+}
+
+template <bool TN, int FM, int FN, int EPI>
+static cudaError_t set_smem_attr() {
+  return cudaFuncSetAttribute(k_gemm<TN, FM, FN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)GemmShape<TN, FM, FN>::SMEM_BYTES);
+}
+
+#define FOR_GEMM_CFGS(X)                                                              \
+  X(2, 1) X(2, 2) X(2, 4) X(4, 1) X(4, 2) X(4, 4) X(8, 1) X(8, 2) X(8, 4)
+
+static cudaError_t set_all_smem_attrs() {
+  cudaError_t e = cudaSuccess;
+#define SETA(FM, FN)                                                 \
+  if (e == cudaSuccess) e = set_smem_attr<false, FM, FN, EPI_DERIV>(); \
+  if (e == cudaSuccess) e = set_smem_attr<false, FM, FN, EPI_EVAL>();  \
+  if (e == cudaSuccess) e = set_smem_attr<false, FM, FN, EPI_STORE>(); \
+  if (e == cudaSuccess) e = set_smem_attr<true, FM, FN, EPI_STORE>();
+  FOR_GEMM_CFGS(SETA)
+#undef SETA
+  return e;
+}
+
+int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, int k_, double M_,
+                 double lambda2_, double L_, int device_) {
+  n = n_;
+  p = p_;
+  k = k_;
+  loss = loss_;
+  M = M_;
+  lambda2 = lambda2_;
+  device = device_;
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&ev0_));
+  CK(cudaEventCreate(&ev1_));
+  CK(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device));
+  CK(cudaMallocHost(&hPin_, 4 * sizeof(int)));
+  CK(cudaMalloc(&dX_, sizeof(double) * (size_t)n * p));
+  CK(cudaMalloc(&dy_, sizeof(double) * (size_t)n));
+  CK(cudaMemcpyAsync(dX_, X, sizeof(double) * (size_t)n * p, cudaMemcpyHostToDevice, stream_));
+  CK(cudaMemcpyAsync(dy_, y, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, stream_));
+  CK(cudaMalloc(&dMa_, sizeof(int)));
+  CK(cudaMalloc(&dErr_, sizeof(int)));
+  CK(set_all_smem_attrs());
+  n2_ = next_pow2(std::max(p, 2));
+  const size_t csmem = column_smem_bytes(p, n2_);
+  if (csmem > 200 * 1024) return fail(1, "p too large for the column kernels");
+  CK(cudaFuncSetAttribute(k_prox_fista, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+  CK(cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+  CK(cudaFuncSetAttribute(k_round_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+  CK(cudaFuncSetAttribute(k_prox_standalone, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)csmem));
+  CK(cudaFuncSetAttribute(k_g_standalone, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+  nrb_max_ = (n + 15) / 16;
+  CK(cudaStreamSynchronize(stream_));
+  if (L_ > 0.0) {
+    L = L_;
+  } else {
+    int rc = compute_smoothness(&L);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+int Engine::ensure(int m) {
+  if (m <= mcap_) return 0;
+  int cap = std::max(m, std::max(16, mcap_ * 2));
+  cudaFree(dB_);
+  cudaFree(dV_);
+  cudaFree(dG_);
+  cudaFree(dR_);
+  cudaFree(dPL_);
+  cudaFree(dPC_);
+  cudaFree(dT_);
+  cudaFree(dBest_);
+  cudaFree(dLast_);
+  cudaFree(dState_);
+  cudaFree(dFrozen_);
+  cudaFree(dKbar_);
+  cudaFree(dPf_);
+  cudaFree(dStatus_);
+  cudaFree(dIters_);
+  cudaFree(dAct_);
+  cudaFree(dSup_);
+  cudaFree(dLen_);
+  cudaFree(dJb_);
+  const size_t pm = (size_t)p * cap;
+  CK(cudaMalloc(&dB_, sizeof(double) * pm));
+  CK(cudaMalloc(&dV_, sizeof(double) * pm));
+  CK(cudaMalloc(&dG_, sizeof(double) * pm * nsplit_max_));
+  CK(cudaMalloc(&dR_, sizeof(double) * (size_t)n * cap));
+  CK(cudaMalloc(&dPL_, sizeof(double) * (size_t)nrb_max_ * cap));
+  CK(cudaMalloc(&dPC_, sizeof(double) * (size_t)nrb_max_ * cap));
+  CK(cudaMalloc(&dT_, sizeof(double) * cap));
+  CK(cudaMalloc(&dBest_, sizeof(double) * cap));
+  CK(cudaMalloc(&dLast_, sizeof(double) * cap));
+  CK(cudaMalloc(&dState_, pm));
+  CK(cudaMalloc(&dFrozen_, cap));
+  CK(cudaMalloc(&dKbar_, sizeof(int) * cap));
+  CK(cudaMalloc(&dPf_, sizeof(int) * cap));
+  CK(cudaMalloc(&dStatus_, sizeof(int) * cap));
+  CK(cudaMalloc(&dIters_, sizeof(int) * cap));
+  CK(cudaMalloc(&dAct_, sizeof(int) * cap));
+  CK(cudaMalloc(&dSup_, sizeof(int) * (size_t)cap * std::max(k, 1)));
+  CK(cudaMalloc(&dLen_, sizeof(int) * cap));
+  CK(cudaMalloc(&dJb_, sizeof(int) * cap));
+  mcap_ = cap;
+  return 0;
+}
+
+int Engine::ensure_aux(size_t bytes) {
+  if (bytes <= aux_bytes_) return 0;
+  cudaFree(dAux_);
+  dAux_ = nullptr;
+  size_t cap = std::max(bytes, aux_bytes_ * 2);
+  CK(cudaMalloc(&dAux_, cap));
+  aux_bytes_ = cap;
+  return 0;
+}
+
+void Engine::tic(int kc) {
+  if (timing) cudaEventRecord(ev0_, stream_);
+}
+void Engine::toc(int kc, double flops) {
+  kc_launches[kc] += 1;
+  kc_flops[kc] += flops;
+  if (timing) {
+    cudaEventRecord(ev1_, stream_);
+    cudaEventSynchronize(ev1_);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev0_, ev1_);
+    kc_ms[kc] += ms;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// GEMM planning: BN from the active width, BM so the grid covers the SMs,
+// split-K (TN only) when the tiles alone cannot.
+// ---------------------------------------------------------------------------
+Engine::GemmPlan Engine::plan(int Mr, int K, int ncols, bool allow_split) const {
+  GemmPlan pl;
+  pl.fn = ncols <= 8 ? 1 : (ncols <= 16 ? 2 : 4);
+  const int nt = (ncols + 8 * pl.fn - 1) / (8 * pl.fn);
+  pl.fm = 2;
+  for (int fm : {8, 4}) {
+    const int ctas = ((Mr + 8 * fm - 1) / (8 * fm)) * nt;
+    if (ctas >= sms_) {
+      pl.fm = fm;
+      break;
+    }
+  }
+  const int mt = (Mr + 8 * pl.fm - 1) / (8 * pl.fm);
+  int nsplit = 1;
+  if (allow_split) {
+    const int nkt = (K + kBK - 1) / kBK;
+    while (nsplit < nsplit_max_ && mt * nt * nsplit * 2 <= 2 * sms_ && nkt >= nsplit * 4)
+      nsplit *= 2;
+  }
+  const int nkt = (K + kBK - 1) / kBK;
+  const int kt_per = (nkt + nsplit - 1) / nsplit;
+  pl.ksplit = kt_per * kBK;
+  pl.nsplit = (K + pl.ksplit - 1) / pl.ksplit;
+  if (pl.nsplit < 1) pl.nsplit = 1;
+  pl.grid = dim3(mt, nt, pl.nsplit);
+  return pl;
+}
+
+int Engine::launch_gemm(bool tn, int epi, const GemmPlan& pl, const double* Bsrc, int ldb,
+                        double* C, int ldc, const int* act, const int* d_ncols,
+                        long long split_stride, int part_ld) {
+  GemmArgs g;
+  g.M = tn ? p : n;
+  g.K = tn ? n : p;
+  g.A = dX_;
+  g.lda = n;
+  g.B = Bsrc;
+  g.ldb = ldb;
+  g.C = C;
+  g.ldc = ldc;
+  g.split_stride = split_stride;
+  g.ksplit = pl.ksplit;
+  g.act = act;
+  g.d_ncols = d_ncols;
+  g.y = dy_;
+  g.loss = loss;
+  g.part_loss = dPL_;
+  g.part_conj = dPC_;
+  g.part_ld = part_ld;
+  const dim3 block(kGemmThreads);
+#define LAUNCH_ONE(FM, FN)                                                                    \
+  if (pl.fm == FM && pl.fn == FN) {                                                           \
+    if (tn) {                                                                                 \
+      k_gemm<true, FM, FN, EPI_STORE>                                                         \
+          <<<pl.grid, block, GemmShape<true, FM, FN>::SMEM_BYTES, stream_>>>(g);              \
+    } else if (epi == EPI_DERIV) {                                                            \
+      k_gemm<false, FM, FN, EPI_DERIV>                                                        \
+          <<<pl.grid, block, GemmShape<false, FM, FN>::SMEM_BYTES, stream_>>>(g);             \
+    } else if (epi == EPI_EVAL) {                                                             \
+      k_gemm<false, FM, FN, EPI_EVAL>                                                         \
+          <<<pl.grid, block, GemmShape<false, FM, FN>::SMEM_BYTES, stream_>>>(g);             \
+    } else {                                                                                  \
+      k_gemm<false, FM, FN, EPI_STORE>                                                        \
+          <<<pl.grid, block, GemmShape<false, FM, FN>::SMEM_BYTES, stream_>>>(g);             \
+    }                                                                                         \
+  }
+  FOR_GEMM_CFGS(LAUNCH_ONE)
+#undef LAUNCH_ONE
+  CKL("k_gemm");
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// smoothness_constant (losses.hpp:86-112): start vector from xoshiro256++
+// seeded 0x5eed5eed on the host, GEMVs and reductions on the device.
+// ---------------------------------------------------------------------------
+int Engine::compute_smoothness(double* out) {
+  const double c = loss == kSquared ? 1.0 : 0.25;
+  std::vector<double> v(p);
+  Xoshiro256pp rng(0x5eed5eedULL);
+  for (int j = 0; j < p; ++j) v[j] = rng.uniform() - 0.5;
+  auto vnorm = [&](const std::vector<double>& a) {
+    double s = 0.0;
+    for (double x : a) s += x * x;
+    return std::sqrt(s);
+  };
+  if (vnorm(v) == 0.0) v[0] = 1.0;
+  {
+    const double nv = vnorm(v);
+    for (double& x : v) x /= nv;
+  }
+  if (int rc = ensure_aux(sizeof(double) * ((size_t)2 * p + n + 2))) return rc;
+  double* dv = static_cast<double*>(dAux_);
+  double* dw = dv + p;
+  double* dxv = dw + p;
+  double* dstat = dxv + n;
+  CK(cudaMemcpyAsync(dv, v.data(), sizeof(double) * p, cudaMemcpyHostToDevice, stream_));
+  double estimate = 0.0, stats[2];
+  double result = -1.0;
+  for (int it = 0; it < 100; ++it) {
+    k_gemv_n<<<(n + 255) / 256, 256, 0, stream_>>>(n, p, dX_, dv, dxv);
+    CKL("k_gemv_n");
+    k_gemv_t<<<(p + 7) / 8, 256, 0, stream_>>>(n, p, dX_, dxv, dw);
+    CKL("k_gemv_t");
+    k_power_stats<<<1, 256, 0, stream_>>>(p, dv, dw, dstat);
+    CKL("k_power_stats");
+    CK(cudaMemcpyAsync(stats, dstat, sizeof(stats), cudaMemcpyDeviceToHost, stream_));
+    CK(cudaStreamSynchronize(stream_));
+    const double next = stats[0], wn = stats[1];
+    if (wn == 0.0 || next <= 0.0) {
+      result = 1e-12;
+      break;
+    }
+    k_scale<<<(p + 255) / 256, 256, 0, stream_>>>(p, dw, wn, dv);
+    CKL("k_scale");
+    if (it > 0 && std::fabs(next - estimate) <= 1e-4 * next) {
+      estimate = next;
+      break;
+    }
+    estimate = next;
+  }
+  if (result < 0.0) result = std::max(1.01 * c * estimate, 1e-12);
+  *out = result;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// one proximal-gradient iteration over the active columns
+// (relaxation.hpp:225-244)
+// ---------------------------------------------------------------------------
+int Engine::step(int ma, double eta, double rho, const RelaxParams& cfg) {
+  const GemmPlan p1 = plan(n, p, ma, false);
+  tic(KC_GEMM_NN);
+  if (int rc = launch_gemm(false, EPI_DERIV, p1, dV_, p, dR_, n, dAct_, dMa_, 0, mcap_)) return rc;
+  toc(KC_GEMM_NN, 2.0 * n * p * ma);
+  const GemmPlan p2 = plan(p, n, ma, true);
+  tic(KC_GEMM_TN);
+  if (int rc = launch_gemm(true, EPI_STORE, p2, dR_, n, dG_, p, dAct_, dMa_,
+                           (long long)p * mcap_, mcap_))
+    return rc;
+  toc(KC_GEMM_TN, 2.0 * n * p * ma);
+  cur_nsplit_ = p2.nsplit;
+  RelaxDev r;
+  r.p = p;
+  r.n2 = n2_;
+  r.mcap = mcap_;
+  r.B = dB_;
+  r.V = dV_;
+  r.G = dG_;
+  r.split_stride = (long long)p * mcap_;
+  r.nsplit = p2.nsplit;
+  r.state = dState_;
+  r.kbar = dKbar_;
+  r.pf = dPf_;
+  r.t = dT_;
+  r.best = dBest_;
+  r.last_gap = dLast_;
+  r.frozen = dFrozen_;
+  r.status = dStatus_;
+  r.iters = dIters_;
+  r.act = dAct_;
+  r.d_ma = dMa_;
+  r.d_err = dErr_;
+  r.eta = eta;
+  r.rho = rho;
+  r.M = M;
+  r.lambda2 = lambda2;
+  r.accel = cfg.acceleration;
+  tic(KC_PROX);
+  k_prox_fista<<<ma, kNodeThreads, column_smem_bytes(p, n2_), stream_>>>(r);
+  CKL("k_prox_fista");
+  toc(KC_PROX, 0.0);
+  return 0;
+}
+
+// evaluate_bounds (relaxation.hpp:194-221) + active-list compaction
+int Engine::evaluate(int ma, double eta, double rho, const RelaxParams& cfg, int iter, double thr,
+                     double* trace, int eval_idx) {
+  const GemmPlan p1 = plan(n, p, ma, false);
+  tic(KC_GEMM_NN);
+  if (int rc = launch_gemm(false, EPI_EVAL, p1, dB_, p, dR_, n, dAct_, dMa_, 0, mcap_)) return rc;
+  toc(KC_GEMM_NN, 2.0 * n * p * ma);
+  const GemmPlan p2 = plan(p, n, ma, true);
+  tic(KC_GEMM_TN);
+  if (int rc = launch_gemm(true, EPI_STORE, p2, dR_, n, dG_, p, dAct_, dMa_,
+                           (long long)p * mcap_, mcap_))
+    return rc;
+  toc(KC_GEMM_TN, 2.0 * n * p * ma);
+  RelaxDev r;
+  r.p = p;
+  r.n2 = n2_;
+  r.mcap = mcap_;
+  r.B = dB_;
+  r.V = dV_;
+  r.G = dG_;
+  r.split_stride = (long long)p * mcap_;
+  r.nsplit = p2.nsplit;
+  r.state = dState_;
+  r.kbar = dKbar_;
+  r.pf = dPf_;
+  r.t = dT_;
+  r.best = dBest_;
+  r.last_gap = dLast_;
+  r.frozen = dFrozen_;
+  r.status = dStatus_;
+  r.iters = dIters_;
+  r.act = dAct_;
+  r.d_ma = dMa_;
+  r.d_err = dErr_;
+  r.eta = eta;
+  r.rho = rho;
+  r.M = M;
+  r.lambda2 = lambda2;
+  r.accel = cfg.acceleration;
+  EvalArgs e;
+  e.part_loss = dPL_;
+  e.part_conj = dPC_;
+  e.nrb = p1.grid.x;
+  e.part_ld = mcap_;
+  e.iter = iter;
+  e.prune_threshold = thr;
+  e.gap_tolerance = cfg.gap_tolerance;
+  e.trace = trace;
+  e.eval_idx = eval_idx;
+  tic(KC_EVAL);
+  k_eval<<<ma, kNodeThreads, column_smem_bytes(p, n2_), stream_>>>(r, e);
+  CKL("k_eval");
+  k_compact<<<1, 1024, 0, stream_>>>(dAct_, dMa_, dFrozen_);
+  CKL("k_compact");
+  toc(KC_EVAL, 0.0);
+  CK(cudaMemcpyAsync(hPin_, dMa_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+  CK(cudaMemcpyAsync(hPin_ + 1, dErr_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+  CK(cudaStreamSynchronize(stream_));
+  if (hPin_[1] != 0x7fffffff) {
+    return fail(2, "relaxation: non-finite iterate in column " + std::to_string(hPin_[1]));
+  }
+  return 0;
+}
+
+int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_trace,
+                           PassResult& out, bool round_select, const int* d_one_off,
+                           const int* d_one_idx) {
+  const double eta = 1.0 / L;  // relaxation.hpp:177-180
+  const double rho = 1.0 / (2.0 * eta * lambda2);
+  const int max_evals = cfg.max_iterations / std::max(1, cfg.check_interval) + 2;
+  double* dTrace = nullptr;
+  if (want_trace) {
+    CK(cudaMalloc(&dTrace, sizeof(double) * (size_t)max_evals * mcap_));
+    CK(cudaMemsetAsync(dTrace, 0xff, sizeof(double) * (size_t)max_evals * mcap_, stream_));
+  }
+  const int big = 0x7fffffff;
+  CK(cudaMemcpyAsync(dErr_, &big, sizeof(int), cudaMemcpyHostToDevice, stream_));
+  CK(cudaMemcpyAsync(dMa_, &m, sizeof(int), cudaMemcpyHostToDevice, stream_));
+  int iter = 0, last_eval = 0, ma = m, n_evals = 0;
+  long long node_its = 0;
+  int rc = 0;
+  while (iter < cfg.max_iterations && ma > 0) {
+    const int to_check = cfg.check_interval - iter % cfg.check_interval;
+    const int nsteps = std::min(to_check, cfg.max_iterations - iter);
+    for (int s = 0; s < nsteps; ++s) {
+      if ((rc = step(ma, eta, rho, cfg))) goto done;
+    }
+    node_its += (long long)nsteps * ma;
+    iter += nsteps;
+    if (iter % cfg.check_interval == 0) {
+      if ((rc = evaluate(ma, eta, rho, cfg, iter, thr, dTrace, n_evals))) goto done;
+      ++n_evals;
+      last_eval = iter;
+      ma = hPin_[0];
+    }
+  }
+  if (ma > 0 && last_eval != iter) {
+    if ((rc = evaluate(ma, eta, rho, cfg, iter, thr, dTrace, n_evals))) goto done;
+    ++n_evals;
+  }
+  out.iterations = iter;
+  out.node_iterations = node_its;
+  out.beta.resize((size_t)p * m);
+  out.bounds.resize(m);
+  out.status.resize(m);
+  out.iters.resize(m);
+  if (round_select) {
+    k_round_select<<<m, kNodeThreads, column_smem_bytes(p, n2_), stream_>>>(
+        p, n2_, std::max(k, 1), dB_, dState_, dKbar_, d_one_off, d_one_idx, dSup_, dLen_, dJb_);
+    CKL("k_round_select");
+    out.sup.resize((size_t)m * std::max(k, 1));
+    out.len.resize(m);
+    out.jbranch.resize(m);
+    CK(cudaMemcpyAsync(out.sup.data(), dSup_, sizeof(int) * out.sup.size(), cudaMemcpyDeviceToHost,
+                       stream_));
+    CK(cudaMemcpyAsync(out.len.data(), dLen_, sizeof(int) * m, cudaMemcpyDeviceToHost, stream_));
+    CK(cudaMemcpyAsync(out.jbranch.data(), dJb_, sizeof(int) * m, cudaMemcpyDeviceToHost,
+                       stream_));
+  }
+  CK(cudaMemcpyAsync(out.beta.data(), dB_, sizeof(double) * (size_t)p * m, cudaMemcpyDeviceToHost,
+                     stream_));
+  CK(cudaMemcpyAsync(out.bounds.data(), dBest_, sizeof(double) * m, cudaMemcpyDeviceToHost,
+                     stream_));
+  CK(cudaMemcpyAsync(out.status.data(), dStatus_, sizeof(int) * m, cudaMemcpyDeviceToHost,
+                     stream_));
+  CK(cudaMemcpyAsync(out.iters.data(), dIters_, sizeof(int) * m, cudaMemcpyDeviceToHost, stream_));
+  out.n_evals = n_evals;
+  if (want_trace) {
+    out.trace.resize((size_t)n_evals * m);
+    for (int e = 0; e < n_evals; ++e)
+      CK(cudaMemcpyAsync(out.trace.data() + (size_t)e * m, dTrace + (size_t)e * mcap_,
+                         sizeof(double) * m, cudaMemcpyDeviceToHost, stream_));
+  }
+  CK(cudaStreamSynchronize(stream_));
+done:
+  if (dTrace) cudaFree(dTrace);
+  return rc;
+}
+
+int Engine::relax_raw(int m, const RelaxParams& cfg, double thr, const uint8_t* state,
+                      const int32_t* kbar, const double* warm, bool trace, PassResult& out) {
+  if (m <= 0) return fail(1, "solve_batch_relaxation: empty batch");
+  if (int rc = ensure(m)) return rc;
+  CK(cudaMemcpyAsync(dState_, state, (size_t)p * m, cudaMemcpyHostToDevice, stream_));
+  CK(cudaMemcpyAsync(dKbar_, kbar, sizeof(int) * m, cudaMemcpyHostToDevice, stream_));
+  CK(cudaMemcpyAsync(dB_, warm, sizeof(double) * (size_t)p * m, cudaMemcpyHostToDevice, stream_));
+  k_init_cols<<<m, kNodeThreads, 0, stream_>>>(p, m, dState_, dPf_, dB_, dV_, dT_, dBest_, dLast_,
+                                              dFrozen_, dStatus_, dIters_, dAct_,
+                                              cfg.max_iterations);
+  CKL("k_init_cols");
+  return relax_uploaded(m, cfg, thr, trace, out, false, nullptr, nullptr);
+}
+
+int Engine::relax_lists(const BatchLists& L_, const double* warm, const RelaxParams& cfg,
+                        double thr, bool trace, PassResult& out) {
+  const int m = L_.m;
+  if (m <= 0) return fail(1, "solve_batch_relaxation: empty batch");
+  if (int rc = ensure(m)) return rc;
+  const size_t nz = L_.z_idx.size(), no = L_.o_idx.size();
+  const size_t ints = (size_t)(m + 1) * 2 + nz + no;
+  const size_t bytes = sizeof(double) * (size_t)p * m + sizeof(int) * (ints + 4);
+  if (int rc = ensure_aux(bytes)) return rc;
+  double* dWarm = static_cast<double*>(dAux_);
+  int* dz_off = reinterpret_cast<int*>(dWarm + (size_t)p * m);
+  int* do_off = dz_off + (m + 1);
+  int* dz_idx = do_off + (m + 1);
+  int* do_idx = dz_idx + nz;
+  CK(cudaMemcpyAsync(dWarm, warm, sizeof(double) * (size_t)p * m, cudaMemcpyHostToDevice, stream_));
+  CK(cudaMemcpyAsync(dz_off, L_.z_off.data(), sizeof(int) * (m + 1), cudaMemcpyHostToDevice,
+                     stream_));
+  CK(cudaMemcpyAsync(do_off, L_.o_off.data(), sizeof(int) * (m + 1), cudaMemcpyHostToDevice,
+                     stream_));
+  if (nz)
+    CK(cudaMemcpyAsync(dz_idx, L_.z_idx.data(), sizeof(int) * nz, cudaMemcpyHostToDevice, stream_));
+  if (no)
+    CK(cudaMemcpyAsync(do_idx, L_.o_idx.data(), sizeof(int) * no, cudaMemcpyHostToDevice, stream_));
+  k_pack<<<m, 256, 0, stream_>>>(p, k, m, dz_off, dz_idx, do_off, do_idx, dState_, dKbar_, dPf_,
+                                 dWarm, dB_, dV_, dT_, dBest_, dLast_, dFrozen_, dStatus_, dIters_,
+                                 dAct_, cfg.max_iterations);
+  CKL("k_pack");
+  return relax_uploaded(m, cfg, thr, trace, out, true, do_off, do_idx);
+}
+
+int Engine::round_select(int m, const double* beta, const uint8_t* state, const int32_t* kbar,
+                         const int32_t* one_off, const int32_t* one_idx, int32_t* sup,
+                         int32_t* len, int32_t* jb) {
+  if (m <= 0) return 0;
+  if (int rc = ensure(m)) return rc;
+  const int no = one_off ? one_off[m] : 0;
+  if (int rc = ensure_aux(sizeof(int) * ((size_t)m + 1 + no + 1))) return rc;
+  int* d_off = static_cast<int*>(dAux_);
+  int* d_idx = d_off + m + 1;
+  CK(cudaMemcpyAsync(dB_, beta, sizeof(double) * (size_t)p * m, cudaMemcpyHostToDevice, stream_));
+  CK(cudaMemcpyAsync(dState_, state, (size_t)p * m, cudaMemcpyHostToDevice, stream_));
+  CK(cudaMemcpyAsync(dKbar_, kbar, sizeof(int) * m, cudaMemcpyHostToDevice, stream_));
+  if (one_off) {
+    CK(cudaMemcpyAsync(d_off, one_off, sizeof(int) * (m + 1), cudaMemcpyHostToDevice, stream_));
+    if (no)
+      CK(cudaMemcpyAsync(d_idx, one_idx, sizeof(int) * no, cudaMemcpyHostToDevice, stream_));
+  }
+  k_round_select<<<m, kNodeThreads, column_smem_bytes(p, n2_), stream_>>>(
+      p, n2_, std::max(k, 1), dB_, dState_, dKbar_, one_off ? d_off : nullptr,
+      one_off ? d_idx : nullptr, dSup_, dLen_, dJb_);
+  CKL("k_round_select");
+  if (sup)
+    CK(cudaMemcpyAsync(sup, dSup_, sizeof(int) * (size_t)m * std::max(k, 1),
+                       cudaMemcpyDeviceToHost, stream_));
+  if (len) CK(cudaMemcpyAsync(len, dLen_, sizeof(int) * m, cudaMemcpyDeviceToHost, stream_));
+  if (jb) CK(cudaMemcpyAsync(jb, dJb_, sizeof(int) * m, cudaMemcpyDeviceToHost, stream_));
+  CK(cudaStreamSynchronize(stream_));
+  return 0;
+}
+
+// reoptimize_supports (primal_heuristics.hpp:174-227)
+int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coef, double* obj) {
+  if (nsup <= 0) return 0;
+  const int tot = offsets[nsup];
+  int qmax = 0;
+  for (int s = 0; s < nsup; ++s) qmax = std::max(qmax, offsets[s + 1] - offsets[s]);
+  const size_t bytes = sizeof(double) * ((size_t)nsup * n + tot + nsup + 2) +
+                       sizeof(int) * ((size_t)nsup + 1 + tot + 2);
+  if (int rc = ensure_aux(bytes)) return rc;
+  double* d_scr = static_cast<double*>(dAux_);
+  double* d_coef = d_scr + (size_t)nsup * n;
+  double* d_obj = d_coef + tot + 1;
+  int* d_off = reinterpret_cast<int*>(d_obj + nsup + 1);
+  int* d_idx = d_off + nsup + 1;
+  CK(cudaMemcpyAsync(d_off, offsets, sizeof(int) * (nsup + 1), cudaMemcpyHostToDevice, stream_));
+  if (tot) CK(cudaMemcpyAsync(d_idx, idx, sizeof(int) * tot, cudaMemcpyHostToDevice, stream_));
+  const double step = 1.0 / (L + 2.0 * lambda2);
+  const size_t smem = sizeof(double) * (size_t)(kReoptThreads / 32 + 2) * std::max(qmax, 1);
+  if (smem > 48 * 1024) {
+    CK(cudaFuncSetAttribute(k_reopt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  tic(KC_REOPT);
+  k_reopt<<<nsup, kReoptThreads, smem, stream_>>>(n, dX_, dy_, loss, M, lambda2, step, d_off, d_idx,
+                                                  d_scr, d_coef, d_obj);
+  CKL("k_reopt");
+  toc(KC_REOPT, 0.0);
+  if (tot) CK(cudaMemcpyAsync(coef, d_coef, sizeof(double) * tot, cudaMemcpyDeviceToHost, stream_));
+  CK(cudaMemcpyAsync(obj, d_obj, sizeof(double) * nsup, cudaMemcpyDeviceToHost, stream_));
+  CK(cudaStreamSynchronize(stream_));
+  return 0;
+}
+
+int Engine::gemm_probe(int trans, int m, const double* Bh, double* Ch) {
+  if (m <= 0) return 0;
+  if (int rc = ensure(m)) return rc;
+  const int K = trans ? n : p, Mo = trans ? p : n;
+  if (int rc = ensure_aux(sizeof(double) * ((size_t)K * m + (size_t)Mo * m * nsplit_max_) + 64))
+    return rc;
+  double* dBin = static_cast<double*>(dAux_);
+  double* dC = dBin + (size_t)K * m;
+  CK(cudaMemcpyAsync(dBin, Bh, sizeof(double) * (size_t)K * m, cudaMemcpyHostToDevice, stream_));
+  CK(cudaMemcpyAsync(dMa_, &m, sizeof(int), cudaMemcpyHostToDevice, stream_));
+  const GemmPlan pl = plan(Mo, K, m, trans != 0);
+  if (int rc = launch_gemm(trans != 0, EPI_STORE, pl, dBin, K, dC, Mo, nullptr, dMa_,
+                           (long long)Mo * m, m))
+    return rc;
+  std::vector<double> slabs((size_t)Mo * m * pl.nsplit);
+  CK(cudaMemcpyAsync(slabs.data(), dC, sizeof(double) * slabs.size(), cudaMemcpyDeviceToHost,
+                     stream_));
+  CK(cudaStreamSynchronize(stream_));
+  for (size_t e = 0; e < (size_t)Mo * m; ++e) {
+    double s = slabs[e];
+    for (int t = 1; t < pl.nsplit; ++t) s += slabs[(size_t)t * Mo * m + e];
+    Ch[e] = s;
+  }
+  return 0;
+}
+
+}  // namespace bnbg
+
+// ===========================================================================
+// stateless kernel entry points (prox_kernel.hpp test surface)
+// ===========================================================================
+#include "../../include/bnbg.h"
+
+namespace {
+
+struct DevScratch {
+  std::vector<void*> ptrs;
+  ~DevScratch() {
+    for (void* q : ptrs) cudaFree(q);
+  }
+  template <class T>
+  T* alloc(size_t count, cudaError_t& e) {
+    void* q = nullptr;
+    if (e == cudaSuccess) e = cudaMalloc(&q, sizeof(T) * std::max<size_t>(count, 1));
+    if (e == cudaSuccess) ptrs.push_back(q);
+    return static_cast<T*>(q);
+  }
+};
+
+thread_local std::string g_stateless_err;
+
+int stateless_column_op(int device, int kind, int mode, int p, int m, const double* in,
+                        const uint8_t* state, const int32_t* kbar, double w, double M,
+                        double* out) {
+  using namespace bnbg;
+  if (p <= 0 || m <= 0) return BNBG_OK;
+  cudaError_t e = cudaSetDevice(device);
+  DevScratch s;
+  const int n2 = next_pow2(std::max(p, 2));
+  const size_t smem = column_smem_bytes(p, n2);
+  double* din = s.alloc<double>((size_t)p * m, e);
+  uint8_t* dst = s.alloc<uint8_t>((size_t)p * m, e);
+  int* dkb = s.alloc<int>(m, e);
+  const size_t outn = kind == 0 ? (size_t)p * m : (size_t)m;
+  double* dout = s.alloc<double>(outn, e);
+  if (e == cudaSuccess) e = cudaMemcpy(din, in, sizeof(double) * (size_t)p * m, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dst, state, (size_t)p * m, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dkb, kbar, sizeof(int) * m, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && kind == 0) {
+    e = cudaFuncSetAttribute(k_prox_standalone, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) {
+      k_prox_standalone<<<m, kNodeThreads, smem>>>(mode, p, n2, din, dst, dkb, w, M, dout);
+      e = cudaGetLastError();
+    }
+  } else if (e == cudaSuccess) {
+    e = cudaFuncSetAttribute(k_g_standalone, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) {
+      k_g_standalone<<<m, kNodeThreads, smem>>>(mode, p, n2, din, dst, dkb, M, dout);
+      e = cudaGetLastError();
+    }
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out, dout, sizeof(double) * outn, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    g_stateless_err = std::string("CUDA error: ") + cudaGetErrorString(e);
+    return BNBG_CUDA_ERROR;
+  }
+  return BNBG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bnbg_prox_step(int device, int p, int m, const double* U, double eta, double lambda2,
+                   const uint8_t* state, const int32_t* kbar, double M, double* out) {
+  if (!(eta > 0.0) || !(lambda2 > 0.0)) return BNBG_INPUT_ERROR;  // prox_kernel.hpp:288-289
+  const double rho = 1.0 / (2.0 * eta * lambda2);
+  return stateless_column_op(device, 0, 0, p, m, U, state, kbar, rho, M, out);
+}
+
+int bnbg_conjugate_prox(int device, int p, int m, const double* U_scaled, double weight,
+                        const uint8_t* state, const int32_t* kbar, double M, double* out) {
+  return stateless_column_op(device, 0, 1, p, m, U_scaled, state, kbar, weight, M, out);
+}
+
+int bnbg_g_value(int device, int p, int m, const double* beta, const uint8_t* state,
+                 const int32_t* kbar, double M, double* out) {
+  return stateless_column_op(device, 1, 0, p, m, beta, state, kbar, 0.0, M, out);
+}
+
+int bnbg_g_conjugate(int device, int p, int m, const double* q, const uint8_t* state,
+                     const int32_t* kbar, double M, double* out) {
+  return stateless_column_op(device, 1, 1, p, m, q, state, kbar, 0.0, M, out);
+}
+
+}  // extern "C"

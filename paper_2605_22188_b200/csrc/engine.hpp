@@ -1,0 +1,123 @@
+// engine.hpp -- one GPU's node-processing engine (host side of the seam).
+//
+// Owns the device-resident instance (X column-major, y), the batch
+// workspaces sized for the widest batch seen, and the stream.  The relaxation
+// loop runs entirely on the device between bound evaluations; the host reads
+// back one integer (the active-column count) per check_interval iterations,
+// exactly when the reference's active count can change
+// (relaxation.hpp:224-250).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+namespace bnbg {
+
+struct RelaxParams {
+  int max_iterations = 2000;
+  double gap_tolerance = 1e-6;
+  int check_interval = 10;
+  int acceleration = 1;
+};
+
+// Host-side batch description in CSR form (one entry per node/column).
+struct BatchLists {
+  int m = 0;
+  std::vector<int> z_off, z_idx;  // J0 lists
+  std::vector<int> o_off, o_idx;  // J1 lists (construction order)
+};
+
+struct PassResult {
+  std::vector<double> beta;   // p x m
+  std::vector<double> bounds; // m
+  std::vector<int> status, iters;
+  std::vector<int> sup, len, jbranch;  // m x k, m, m
+  std::vector<double> trace;  // n_evals x m (NaN where not evaluated)
+  int n_evals = 0;
+  long long iterations = 0;       // loop iterations run
+  long long node_iterations = 0;  // sum over columns of iterations
+};
+
+enum KernelClass { KC_GEMM_NN = 0, KC_GEMM_TN, KC_PROX, KC_EVAL, KC_REOPT, KC_OTHER, KC_COUNT };
+
+class Engine {
+ public:
+  Engine() = default;
+  ~Engine();
+  int init(const double* X, const double* y, int n, int p, int loss, int k, double M,
+           double lambda2, double L, int device);
+
+  // losses.hpp:86-112 on the device
+  int compute_smoothness(double* out);
+
+  // solve_batch_relaxation over columns already uploaded (state/kbar/B)
+  int relax_uploaded(int m, const RelaxParams& cfg, double prune_threshold, bool trace,
+                     PassResult& out, bool round_select, const int* d_one_off,
+                     const int* d_one_idx);
+  // bnbg_relax_batch: raw state/kbar/warm from the host
+  int relax_raw(int m, const RelaxParams& cfg, double prune_threshold, const uint8_t* state,
+                const int32_t* kbar, const double* warm, bool trace, PassResult& out);
+  // one BnB pass of lower bounds + rounding + branch selection from CSR lists
+  int relax_lists(const BatchLists& lists, const double* warm, const RelaxParams& cfg,
+                  double prune_threshold, bool trace, PassResult& out);
+  // reoptimize_supports (CSR)
+  int reoptimize(int nsup, const int* offsets, const int* idx, double* coef, double* obj);
+  int round_select(int m, const double* beta, const uint8_t* state, const int32_t* kbar,
+                   const int32_t* one_off, const int32_t* one_idx, int32_t* sup, int32_t* len,
+                   int32_t* jb);
+  int gemm_probe(int trans, int m, const double* B, double* C);
+
+  int n = 0, p = 0, k = 0, loss = 0, device = 0;
+  double M = 1.0, lambda2 = 1.0, L = 0.0;
+  long long launches = 0;
+  bool timing = false;
+  double kc_ms[KC_COUNT] = {0};
+  double kc_flops[KC_COUNT] = {0};
+  long long kc_launches[KC_COUNT] = {0};
+  std::string err;
+
+ private:
+  int ensure(int m);
+  int ensure_aux(size_t bytes);
+  int fail(int code, const std::string& msg);
+  int cuda_fail(cudaError_t e, const char* what);
+  int step(int ma, double eta, double rho, const RelaxParams& cfg);
+  int evaluate(int ma, double eta, double rho, const RelaxParams& cfg, int iter, double thr,
+               double* trace, int eval_idx);
+  struct GemmPlan {
+    int fm, fn, nsplit, ksplit;
+    dim3 grid;
+  };
+  GemmPlan plan(int M, int K, int ncols, bool allow_split) const;
+  int launch_gemm(bool tn, int epi, const GemmPlan& pl, const double* Bsrc, int ldb, double* C,
+                  int ldc, const int* act, const int* d_ncols, long long split_stride,
+                  int part_ld);
+  void tic(int kc);
+  void toc(int kc, double flops);
+
+  cudaStream_t stream_ = nullptr;
+  cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  int n2_ = 1;
+  int sms_ = 148;
+  int mcap_ = 0;
+  double* dX_ = nullptr;
+  double* dy_ = nullptr;
+  double *dB_ = nullptr, *dV_ = nullptr, *dG_ = nullptr, *dR_ = nullptr;
+  double *dPL_ = nullptr, *dPC_ = nullptr;
+  double *dT_ = nullptr, *dBest_ = nullptr, *dLast_ = nullptr;
+  uint8_t *dState_ = nullptr, *dFrozen_ = nullptr;
+  int *dKbar_ = nullptr, *dPf_ = nullptr, *dStatus_ = nullptr, *dIters_ = nullptr;
+  int *dAct_ = nullptr, *dMa_ = nullptr, *dErr_ = nullptr;
+  int *dSup_ = nullptr, *dLen_ = nullptr, *dJb_ = nullptr;
+  void* dAux_ = nullptr;  // CSR uploads, reopt scratch, trace
+  size_t aux_bytes_ = 0;
+  int* hPin_ = nullptr;   // pinned: [0] ma, [1] err
+  int nsplit_max_ = 8;
+  int nrb_max_ = 1;
+  int cur_nsplit_ = 1;
+  int cur_nrb_ = 1;
+};
+
+}  // namespace bnbg
