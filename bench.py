@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""bench.py -- time-to-certify (0 gap) and BnB nodes/sec on B200.
+
+One "step" = one full certified solve (bnbglm::solve, bnb_engine.hpp:299-309)
+of the BASELINE.json configs[1] workload (c2: synthetic sparse logistic
+regression n=2000, p=500, k=8, rho=0.7, seed 0, M=2, lambda2=1; the other
+configs are parity-test cases).  value = nodes processed / second over the
+timed steps (whole job: all ranks); ms_per_step = time-to-certify.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+--impl reference times the reference algorithm's CPU implementation (the C
+restatement in oracle/, OpenBLAS DGEMM, all host threads) on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (n, p, k, rho, loss, description)
+    "c1": (1000, 100, 5, 0.5, 0, "synthetic sparse linear regression n=1000 p=100 k=5 rho=0.5"),
+    "c2": (2000, 500, 8, 0.7, 1, "synthetic sparse logistic regression n=2000 p=500 k=8 rho=0.7"),
+    "c3": (5000, 2000, 10, 0.9, 0, "synthetic sparse linear regression n=5000 p=2000 k=10 rho=0.9"),
+}
+METRIC = "BnB nodes/sec at time-to-certify (0 gap)"
+FP64_PEAK_TFLOPS = 37.0  # measured DMMA.8x8x4 issue rate on this pool (profiles/r01_fp64_peak.txt)
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def _ncu_traffic(kernel_class):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(kernel_class, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def run_reference(args, spec, rank):
+    """Reference arm: the CPU implementation of the path on the host cores."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    n, p, k, rho, loss, desc = spec
+    O.build()
+    threads = os.cpu_count() or 1
+    blas = O.use_openblas(threads)
+    inst = O.generate(n, p, k, rho, loss, 5.0, 0, 2.0, 1.0)
+    cfg_full = O.solver_cfg(workers=threads)
+    # untimed warm-up: bounded 1 s samples
+    for _ in range(args.warmup):
+        O.solve(inst, O.solver_cfg(workers=threads, time_limit=1.0))
+    # one probe run decides whether K full certifies fit in ~4 minutes
+    t0 = time.perf_counter()
+    first = O.solve(inst, cfg_full)
+    t_full = time.perf_counter() - t0
+    results = [(first.nodes_processed, t_full, first.status)]
+    budget = 240.0
+    limit = math.inf if t_full * args.steps <= budget else budget / args.steps
+    for _ in range(args.steps - 1):
+        t0 = time.perf_counter()
+        c = O.solve(inst, O.solver_cfg(workers=threads, time_limit=limit))
+        results.append((c.nodes_processed, time.perf_counter() - t0, c.status))
+    nodes = sum(r[0] for r in results)
+    secs = sum(r[1] for r in results)
+    value = nodes / secs
+    sample = (f"{args.steps} x full certify of {args.config} ({first.nodes_processed} nodes, "
+              f"{t_full:.1f} s each)" if limit == math.inf else
+              f"1 full certify ({t_full:.1f} s) + {args.steps - 1} samples capped at {limit:.0f} s")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "nodes/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (generate_synthetic, seed 0)",
+        "config": {"workload": f"{args.config}: {desc}, certify to 0 gap", "batch_size": "auto",
+                   "time_to_certify_s": t_full},
+        "cpu_baseline": {"value": value, "unit": "nodes/s", "cores": threads, "kind": "port",
+                         "sample": sample + ("; OpenBLAS DGEMM" if blas else "; C loops")},
+        "e2e": {"value": value, "unit": "nodes/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(spec, args):
+    from oracle import oracle as O
+    n, p, k, rho, loss, desc = spec
+    O.build()
+    threads = os.cpu_count() or 1
+    blas = O.use_openblas(threads)
+    inst = O.generate(n, p, k, rho, loss, 5.0, 0, 2.0, 1.0)
+    limit = args.cpu_seconds
+    t0 = time.perf_counter()
+    c = O.solve(inst, O.solver_cfg(workers=threads, time_limit=limit))
+    secs = time.perf_counter() - t0
+    return {"value": c.nodes_processed / secs, "unit": "nodes/s", "cores": threads, "kind": "port",
+            "sample": (f"one certify of {args.config} on {threads} threads"
+                       + (" (OpenBLAS DGEMM)" if blas else "") +
+                       f": {c.nodes_processed} nodes in {secs:.1f} s, status {c.status}"),
+            "time_to_certify_s": secs if c.status == "optimal" else None,
+            "optimal_value": c.optimal_value, "support": c.support}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=120.0)
+    args = ap.parse_args()
+    spec = CONFIGS[args.config]
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+
+    if args.impl == "reference":
+        run_reference(args, spec, rank)
+        return
+
+    import numpy as np
+    import torch
+    import paper_2605_22188_b200 as P
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, p, k, rho, loss, desc = spec
+    inst, _ = P.generate_synthetic(P.GeneratorSpec(n=n, p=p, k=k, correlation=rho, loss=loss,
+                                                   seed=0, M=2.0, lambda2=1.0))
+    cfg = P.SolverConfig()
+    eng = P.Engine(inst, device=local)  # X, y resident in HBM before timing
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > L2
+
+    for _ in range(args.warmup):
+        eng.solve(cfg)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    launches0 = eng.kernel_launches()
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier()
+    total_ms, nodes, certs = 0.0, 0, []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        cert = eng.solve(cfg)
+        e1.record()
+        torch.cuda.synchronize()
+        total_ms += e0.elapsed_time(e1)
+        nodes += cert.nodes_processed
+        certs.append(cert)
+    barrier()
+    clocks = sampler.stop()
+    launches = eng.kernel_launches() - launches0
+
+    t = torch.tensor([total_ms, float(nodes)], dtype=torch.float64, device="cuda")
+    if dist:
+        tmax = t.clone()
+        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum[1:], op=dist.ReduceOp.SUM)
+        total_ms_max, nodes_all = float(tmax[0]), float(tsum[1])
+    else:
+        total_ms_max, nodes_all = total_ms, float(nodes)
+    value = nodes_all / (total_ms_max / 1e3)
+
+    # roofline: one extra (untimed) certify with per-launch CUDA events on the engine stream
+    eng.set_timing(True)
+    before = eng.kernel_stats()
+    prof_cert = eng.solve(cfg)
+    after = eng.kernel_stats()
+    eng.set_timing(False)
+    delta = {kc: tuple(a - b for a, b in zip(after[kc], before[kc])) for kc in after}
+    dom = max(delta, key=lambda kc: delta[kc][0])
+    ms, fl, ln = delta[dom]
+    peaks = _load_peaks()
+    if dom.startswith("gemm"):
+        achieved = fl / (ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+                "peak_source": "measured FP64 DMMA issue rate (profiles/r01_fp64_peak.txt); "
+                               "MEASURED_PEAKS.json has no fp64 entry",
+                "algorithmic": "2*n*p flops per active column per launch"}
+    else:
+        node_its = prof_cert.node_iterations
+        bytes_ = 41.0 * p * node_its if dom == "prox_fista" else float("nan")
+        achieved = bytes_ / (ms / 1e3) / 1e9
+        peak = peaks.get("hbm_gbs", 6650.0)
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "algorithmic": "41*p bytes per node-iteration"}
+    roof["traffic"] = _ncu_traffic(dom)
+    roof["avg_launch_us"] = 1e3 * ms / max(ln, 1)
+    roof["share_of_step"] = ms / max(1e-9, 1e3 * prof_cert.profile.total_seconds)
+    roof["kernel_ms"] = {kc: round(v[0], 3) for kc, v in delta.items()}
+
+    # e2e: the public API from host arrays (instance upload, solve, certificate readback)
+    eng_h2d0, eng_d2h0 = 0, 0
+    e2e_ms, e2e_nodes, h2d, d2h = 0.0, 0, 0, 0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with P.Engine(inst, device=local) as e2:
+            c2 = e2.solve(cfg)
+            bi, bo = e2.transfer_bytes()
+        torch.cuda.synchronize()
+        e2e_ms += 1e3 * (time.perf_counter() - t0)
+        e2e_nodes += c2.nodes_processed
+        h2d += bi
+        d2h += bo + 8 * (2 * len(c2.support) + 16)
+    if dist:
+        te = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_ms = float(te[0])
+    e2e_value = e2e_nodes * world / (e2e_ms / 1e3)
+
+    base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        base = cpu_baseline(spec, args)
+        if base.get("support") is not None and base["support"] != certs[0].support:
+            base["support_mismatch"] = True
+
+    if rank == 0:
+        c0 = certs[0]
+        line = {
+            "metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (generate_synthetic, seed 0, problem.hpp:70-132)",
+            "config": {"workload": f"{args.config}: {desc}, certify to 0 gap",
+                       "n": n, "p": p, "k": k, "rho": rho, "loss": "logistic" if loss else "squared",
+                       "batch_size": c0.batch_size_used, "parallelism": f"replicas{world}",
+                       "l2": "flushed (256 MiB write) before every step",
+                       "time_to_certify_s": total_ms_max / args.steps / 1e3,
+                       "nodes_per_certify": c0.nodes_processed, "lb_batches": c0.lb_batches,
+                       "relax_iterations": c0.relax_iterations,
+                       "node_iterations": c0.node_iterations,
+                       "optimal_value": c0.optimal_value, "support": c0.support,
+                       "profile": {"lower_bound_s": c0.profile.lower_bound_seconds,
+                                   "reoptimization_s": c0.profile.reoptimization_seconds,
+                                   "transfer_s": c0.profile.transfer_seconds,
+                                   "branch_generate_s": c0.profile.branch_generate_seconds}},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "roofline": roof,
+            "e2e": {"value": e2e_value, "unit": "nodes/s",
+                    "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+                    "time_to_certify_s": e2e_ms / args.steps / 1e3},
+            "cpu_baseline": base,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -190,6 +190,13 @@ long long bnbg_kernel_launches(const bnbg_handle* h);
 int bnbg_gemm_stats(const bnbg_handle* h, double* gemm_ms, double* gemm_flops,
                     long long* gemm_launches);
 void bnbg_set_timing(bnbg_handle* h, int enabled);
+/* Per kernel class (0 GEMM X*V, 1 GEMM X'*R, 2 prox/FISTA, 3 bound evaluation,
+ * 4 re-optimisation): CUDA-event time (ms, only while timing is enabled),
+ * algorithmic FP64 flops and launches. */
+int bnbg_kernel_stats(const bnbg_handle* h, int kernel_class, double* ms, double* flops,
+                      long long* launches);
+/* Host<->device bytes copied by this handle so far. */
+int bnbg_transfer_bytes(const bnbg_handle* h, long long* h2d, long long* d2h);
 
 #ifdef __cplusplus
 }

@@ -356,6 +356,22 @@ class Engine:
     def set_timing(self, on: bool):
         _L.lib().bnbg_set_timing(self._h, int(on))
 
+    KERNEL_CLASSES = ("gemm_xv", "gemm_xtr", "prox_fista", "eval", "reopt")
+
+    def kernel_stats(self):
+        """{class: (ms, flops, launches)} -- ms only while timing is enabled."""
+        out = {}
+        for kc, name in enumerate(self.KERNEL_CLASSES):
+            ms, fl, ln = C.c_double(), C.c_double(), C.c_longlong()
+            _L.lib().bnbg_kernel_stats(self._h, kc, C.byref(ms), C.byref(fl), C.byref(ln))
+            out[name] = (ms.value, fl.value, ln.value)
+        return out
+
+    def transfer_bytes(self):
+        a, b = C.c_longlong(), C.c_longlong()
+        _L.lib().bnbg_transfer_bytes(self._h, C.byref(a), C.byref(b))
+        return a.value, b.value
+
     def gemm_stats(self):
         ms, fl, ln = C.c_double(), C.c_double(), C.c_longlong()
         _L.lib().bnbg_gemm_stats(self._h, C.byref(ms), C.byref(fl), C.byref(ln))

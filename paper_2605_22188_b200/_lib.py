@@ -58,7 +58,7 @@ EXPORTS = [
     "bnbg_select_branch", "bnbg_reoptimize", "bnbg_prox_step", "bnbg_conjugate_prox",
     "bnbg_g_value", "bnbg_g_conjugate", "bnbg_gemm", "bnbg_solve", "bnbg_collect_rashomon",
     "bnbg_pool_size", "bnbg_pool_record", "bnbg_pool_free", "bnbg_kernel_launches",
-    "bnbg_gemm_stats", "bnbg_set_timing",
+    "bnbg_gemm_stats", "bnbg_set_timing", "bnbg_kernel_stats", "bnbg_transfer_bytes",
 ]
 
 
@@ -109,5 +109,7 @@ def lib():
     L.bnbg_gemm_stats.argtypes = [vp, C.POINTER(d), C.POINTER(d), C.POINTER(ll)]
     L.bnbg_set_timing.argtypes = [vp, i]
     L.bnbg_set_timing.restype = None
+    L.bnbg_kernel_stats.argtypes = [vp, i, C.POINTER(d), C.POINTER(d), C.POINTER(ll)]
+    L.bnbg_transfer_bytes.argtypes = [vp, C.POINTER(ll), C.POINTER(ll)]
     _lib = L
     return L

@@ -698,4 +698,20 @@ int bnbg_gemm_stats(const bnbg_handle* h, double* gemm_ms, double* gemm_flops,
 
 void bnbg_set_timing(bnbg_handle* h, int enabled) { h->eng.timing = enabled != 0; }
 
+int bnbg_kernel_stats(const bnbg_handle* h, int kc, double* ms, double* flops,
+                      long long* launches) {
+  if (kc < 0 || kc >= bnbg::KC_COUNT) return BNBG_INPUT_ERROR;
+  const auto& e = h->eng;
+  if (ms) *ms = e.kc_ms[kc];
+  if (flops) *flops = e.kc_flops[kc];
+  if (launches) *launches = e.kc_launches[kc];
+  return BNBG_OK;
+}
+
+int bnbg_transfer_bytes(const bnbg_handle* h, long long* h2d, long long* d2h) {
+  if (h2d) *h2d = h->eng.h2d_bytes;
+  if (d2h) *d2h = h->eng.d2h_bytes;
+  return BNBG_OK;
+}
+
 }  // extern "C"

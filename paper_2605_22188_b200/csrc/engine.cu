@@ -109,8 +109,8 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
   CK(cudaMallocHost(&hPin_, 4 * sizeof(int)));
   CK(cudaMalloc(&dX_, sizeof(double) * (size_t)n * p));
   CK(cudaMalloc(&dy_, sizeof(double) * (size_t)n));
-  CK(cudaMemcpyAsync(dX_, X, sizeof(double) * (size_t)n * p, cudaMemcpyHostToDevice, stream_));
-  CK(cudaMemcpyAsync(dy_, y, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, stream_));
+  if (int rc_ = h2d(dX_, X, sizeof(double) * (size_t)n * p)) return rc_;
+  if (int rc_ = h2d(dy_, y, sizeof(double) * (size_t)n)) return rc_;
   CK(cudaMalloc(&dMa_, sizeof(int)));
   CK(cudaMalloc(&dErr_, sizeof(int)));
   CK(set_all_smem_attrs());
@@ -190,19 +190,55 @@ int Engine::ensure_aux(size_t bytes) {
   return 0;
 }
 
+cudaEvent_t Engine::get_event() {
+  if (!ev_pool_.empty()) {
+    cudaEvent_t e = ev_pool_.back();
+    ev_pool_.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Deferred CUDA-event timing of each kernel class on the engine stream: the
+// pairs are resolved at the next stream synchronisation, so timing does not
+// add host syncs to the loop.
 void Engine::tic(int kc) {
-  if (timing) cudaEventRecord(ev0_, stream_);
+  (void)kc;
+  if (!timing) return;
+  cur_a_ = get_event();
+  cudaEventRecord(cur_a_, stream_);
 }
 void Engine::toc(int kc, double flops) {
   kc_launches[kc] += 1;
   kc_flops[kc] += flops;
-  if (timing) {
-    cudaEventRecord(ev1_, stream_);
-    cudaEventSynchronize(ev1_);
+  if (!timing) return;
+  cudaEvent_t b = get_event();
+  cudaEventRecord(b, stream_);
+  pending_.push_back({cur_a_, b, kc});
+}
+void Engine::resolve_timing() {
+  for (auto& pr : pending_) {
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, ev0_, ev1_);
-    kc_ms[kc] += ms;
+    if (cudaEventElapsedTime(&ms, pr.a, pr.b) == cudaSuccess) kc_ms[pr.kc] += ms;
+    ev_pool_.push_back(pr.a);
+    ev_pool_.push_back(pr.b);
   }
+  pending_.clear();
+}
+
+int Engine::h2d(void* dst, const void* src, size_t bytes) {
+  if (!bytes) return 0;
+  h2d_bytes += (long long)bytes;
+  if (int rc_ = h2d(dst, src, bytes)) return rc_;
+  return 0;
+}
+int Engine::d2h(void* dst, const void* src, size_t bytes) {
+  if (!bytes) return 0;
+  d2h_bytes += (long long)bytes;
+  if (int rc_ = d2h(dst, src, bytes)) return rc_;
+  return 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -305,7 +341,7 @@ int Engine::compute_smoothness(double* out) {
   double* dw = dv + p;
   double* dxv = dw + p;
   double* dstat = dxv + n;
-  CK(cudaMemcpyAsync(dv, v.data(), sizeof(double) * p, cudaMemcpyHostToDevice, stream_));
+  if (int rc_ = h2d(dv, v.data(), sizeof(double) * p)) return rc_;
   double estimate = 0.0, stats[2];
   double result = -1.0;
   for (int it = 0; it < 100; ++it) {
@@ -315,7 +351,7 @@ int Engine::compute_smoothness(double* out) {
     CKL("k_gemv_t");
     k_power_stats<<<1, 256, 0, stream_>>>(p, dv, dw, dstat);
     CKL("k_power_stats");
-    CK(cudaMemcpyAsync(stats, dstat, sizeof(stats), cudaMemcpyDeviceToHost, stream_));
+    if (int rc_ = d2h(stats, dstat, sizeof(stats))) return rc_;
     CK(cudaStreamSynchronize(stream_));
     const double next = stats[0], wn = stats[1];
     if (wn == 0.0 || next <= 0.0) {
@@ -439,9 +475,10 @@ int Engine::evaluate(int ma, double eta, double rho, const RelaxParams& cfg, int
   k_compact<<<1, 1024, 0, stream_>>>(dAct_, dMa_, dFrozen_);
   CKL("k_compact");
   toc(KC_EVAL, 0.0);
-  CK(cudaMemcpyAsync(hPin_, dMa_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
-  CK(cudaMemcpyAsync(hPin_ + 1, dErr_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+  if (int rc_ = d2h(hPin_, dMa_, sizeof(int))) return rc_;
+  if (int rc_ = d2h(hPin_ + 1, dErr_, sizeof(int))) return rc_;
   CK(cudaStreamSynchronize(stream_));
+  resolve_timing();
   if (hPin_[1] != 0x7fffffff) {
     return fail(2, "relaxation: non-finite iterate in column " + std::to_string(hPin_[1]));
   }
@@ -460,8 +497,8 @@ int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_
     CK(cudaMemsetAsync(dTrace, 0xff, sizeof(double) * (size_t)max_evals * mcap_, stream_));
   }
   const int big = 0x7fffffff;
-  CK(cudaMemcpyAsync(dErr_, &big, sizeof(int), cudaMemcpyHostToDevice, stream_));
-  CK(cudaMemcpyAsync(dMa_, &m, sizeof(int), cudaMemcpyHostToDevice, stream_));
+  if (int rc_ = h2d(dErr_, &big, sizeof(int))) return rc_;
+  if (int rc_ = h2d(dMa_, &m, sizeof(int))) return rc_;
   int iter = 0, last_eval = 0, ma = m, n_evals = 0;
   long long node_its = 0;
   int rc = 0;
@@ -497,27 +534,22 @@ int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_
     out.sup.resize((size_t)m * std::max(k, 1));
     out.len.resize(m);
     out.jbranch.resize(m);
-    CK(cudaMemcpyAsync(out.sup.data(), dSup_, sizeof(int) * out.sup.size(), cudaMemcpyDeviceToHost,
-                       stream_));
-    CK(cudaMemcpyAsync(out.len.data(), dLen_, sizeof(int) * m, cudaMemcpyDeviceToHost, stream_));
-    CK(cudaMemcpyAsync(out.jbranch.data(), dJb_, sizeof(int) * m, cudaMemcpyDeviceToHost,
-                       stream_));
+    if (int rc_ = d2h(out.sup.data(), dSup_, sizeof(int) * out.sup.size())) return rc_;
+    if (int rc_ = d2h(out.len.data(), dLen_, sizeof(int) * m)) return rc_;
+    if (int rc_ = d2h(out.jbranch.data(), dJb_, sizeof(int) * m)) return rc_;
   }
-  CK(cudaMemcpyAsync(out.beta.data(), dB_, sizeof(double) * (size_t)p * m, cudaMemcpyDeviceToHost,
-                     stream_));
-  CK(cudaMemcpyAsync(out.bounds.data(), dBest_, sizeof(double) * m, cudaMemcpyDeviceToHost,
-                     stream_));
-  CK(cudaMemcpyAsync(out.status.data(), dStatus_, sizeof(int) * m, cudaMemcpyDeviceToHost,
-                     stream_));
-  CK(cudaMemcpyAsync(out.iters.data(), dIters_, sizeof(int) * m, cudaMemcpyDeviceToHost, stream_));
+  if (int rc_ = d2h(out.beta.data(), dB_, sizeof(double) * (size_t)p * m)) return rc_;
+  if (int rc_ = d2h(out.bounds.data(), dBest_, sizeof(double) * m)) return rc_;
+  if (int rc_ = d2h(out.status.data(), dStatus_, sizeof(int) * m)) return rc_;
+  if (int rc_ = d2h(out.iters.data(), dIters_, sizeof(int) * m)) return rc_;
   out.n_evals = n_evals;
   if (want_trace) {
     out.trace.resize((size_t)n_evals * m);
     for (int e = 0; e < n_evals; ++e)
-      CK(cudaMemcpyAsync(out.trace.data() + (size_t)e * m, dTrace + (size_t)e * mcap_,
-                         sizeof(double) * m, cudaMemcpyDeviceToHost, stream_));
+      if (int rc_ = d2h(out.trace.data() + (size_t)e * m, dTrace + (size_t)e * mcap_, sizeof(double) * m)) return rc_;
   }
   CK(cudaStreamSynchronize(stream_));
+  resolve_timing();
 done:
   if (dTrace) cudaFree(dTrace);
   return rc;
@@ -527,9 +559,9 @@ int Engine::relax_raw(int m, const RelaxParams& cfg, double thr, const uint8_t* 
                       const int32_t* kbar, const double* warm, bool trace, PassResult& out) {
   if (m <= 0) return fail(1, "solve_batch_relaxation: empty batch");
   if (int rc = ensure(m)) return rc;
-  CK(cudaMemcpyAsync(dState_, state, (size_t)p * m, cudaMemcpyHostToDevice, stream_));
-  CK(cudaMemcpyAsync(dKbar_, kbar, sizeof(int) * m, cudaMemcpyHostToDevice, stream_));
-  CK(cudaMemcpyAsync(dB_, warm, sizeof(double) * (size_t)p * m, cudaMemcpyHostToDevice, stream_));
+  if (int rc_ = h2d(dState_, state, (size_t)p * m)) return rc_;
+  if (int rc_ = h2d(dKbar_, kbar, sizeof(int) * m)) return rc_;
+  if (int rc_ = h2d(dB_, warm, sizeof(double) * (size_t)p * m)) return rc_;
   k_init_cols<<<m, kNodeThreads, 0, stream_>>>(p, m, dState_, dPf_, dB_, dV_, dT_, dBest_, dLast_,
                                               dFrozen_, dStatus_, dIters_, dAct_,
                                               cfg.max_iterations);
@@ -551,15 +583,13 @@ int Engine::relax_lists(const BatchLists& L_, const double* warm, const RelaxPar
   int* do_off = dz_off + (m + 1);
   int* dz_idx = do_off + (m + 1);
   int* do_idx = dz_idx + nz;
-  CK(cudaMemcpyAsync(dWarm, warm, sizeof(double) * (size_t)p * m, cudaMemcpyHostToDevice, stream_));
-  CK(cudaMemcpyAsync(dz_off, L_.z_off.data(), sizeof(int) * (m + 1), cudaMemcpyHostToDevice,
-                     stream_));
-  CK(cudaMemcpyAsync(do_off, L_.o_off.data(), sizeof(int) * (m + 1), cudaMemcpyHostToDevice,
-                     stream_));
+  if (int rc_ = h2d(dWarm, warm, sizeof(double) * (size_t)p * m)) return rc_;
+  if (int rc_ = h2d(dz_off, L_.z_off.data(), sizeof(int) * (m + 1))) return rc_;
+  if (int rc_ = h2d(do_off, L_.o_off.data(), sizeof(int) * (m + 1))) return rc_;
   if (nz)
-    CK(cudaMemcpyAsync(dz_idx, L_.z_idx.data(), sizeof(int) * nz, cudaMemcpyHostToDevice, stream_));
+    if (int rc_ = h2d(dz_idx, L_.z_idx.data(), sizeof(int) * nz)) return rc_;
   if (no)
-    CK(cudaMemcpyAsync(do_idx, L_.o_idx.data(), sizeof(int) * no, cudaMemcpyHostToDevice, stream_));
+    if (int rc_ = h2d(do_idx, L_.o_idx.data(), sizeof(int) * no)) return rc_;
   k_pack<<<m, 256, 0, stream_>>>(p, k, m, dz_off, dz_idx, do_off, do_idx, dState_, dKbar_, dPf_,
                                  dWarm, dB_, dV_, dT_, dBest_, dLast_, dFrozen_, dStatus_, dIters_,
                                  dAct_, cfg.max_iterations);
@@ -576,24 +606,24 @@ int Engine::round_select(int m, const double* beta, const uint8_t* state, const 
   if (int rc = ensure_aux(sizeof(int) * ((size_t)m + 1 + no + 1))) return rc;
   int* d_off = static_cast<int*>(dAux_);
   int* d_idx = d_off + m + 1;
-  CK(cudaMemcpyAsync(dB_, beta, sizeof(double) * (size_t)p * m, cudaMemcpyHostToDevice, stream_));
-  CK(cudaMemcpyAsync(dState_, state, (size_t)p * m, cudaMemcpyHostToDevice, stream_));
-  CK(cudaMemcpyAsync(dKbar_, kbar, sizeof(int) * m, cudaMemcpyHostToDevice, stream_));
+  if (int rc_ = h2d(dB_, beta, sizeof(double) * (size_t)p * m)) return rc_;
+  if (int rc_ = h2d(dState_, state, (size_t)p * m)) return rc_;
+  if (int rc_ = h2d(dKbar_, kbar, sizeof(int) * m)) return rc_;
   if (one_off) {
-    CK(cudaMemcpyAsync(d_off, one_off, sizeof(int) * (m + 1), cudaMemcpyHostToDevice, stream_));
+    if (int rc_ = h2d(d_off, one_off, sizeof(int) * (m + 1))) return rc_;
     if (no)
-      CK(cudaMemcpyAsync(d_idx, one_idx, sizeof(int) * no, cudaMemcpyHostToDevice, stream_));
+      if (int rc_ = h2d(d_idx, one_idx, sizeof(int) * no)) return rc_;
   }
   k_round_select<<<m, kNodeThreads, column_smem_bytes(p, n2_), stream_>>>(
       p, n2_, std::max(k, 1), dB_, dState_, dKbar_, one_off ? d_off : nullptr,
       one_off ? d_idx : nullptr, dSup_, dLen_, dJb_);
   CKL("k_round_select");
   if (sup)
-    CK(cudaMemcpyAsync(sup, dSup_, sizeof(int) * (size_t)m * std::max(k, 1),
-                       cudaMemcpyDeviceToHost, stream_));
-  if (len) CK(cudaMemcpyAsync(len, dLen_, sizeof(int) * m, cudaMemcpyDeviceToHost, stream_));
-  if (jb) CK(cudaMemcpyAsync(jb, dJb_, sizeof(int) * m, cudaMemcpyDeviceToHost, stream_));
+    if (int rc_ = d2h(sup, dSup_, sizeof(int) * (size_t)m * std::max(k, 1))) return rc_;
+  if (len) if (int rc_ = d2h(len, dLen_, sizeof(int) * m)) return rc_;
+  if (jb) if (int rc_ = d2h(jb, dJb_, sizeof(int) * m)) return rc_;
   CK(cudaStreamSynchronize(stream_));
+  resolve_timing();
   return 0;
 }
 
@@ -611,8 +641,8 @@ int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coe
   double* d_obj = d_coef + tot + 1;
   int* d_off = reinterpret_cast<int*>(d_obj + nsup + 1);
   int* d_idx = d_off + nsup + 1;
-  CK(cudaMemcpyAsync(d_off, offsets, sizeof(int) * (nsup + 1), cudaMemcpyHostToDevice, stream_));
-  if (tot) CK(cudaMemcpyAsync(d_idx, idx, sizeof(int) * tot, cudaMemcpyHostToDevice, stream_));
+  if (int rc_ = h2d(d_off, offsets, sizeof(int) * (nsup + 1))) return rc_;
+  if (tot) if (int rc_ = h2d(d_idx, idx, sizeof(int) * tot)) return rc_;
   const double step = 1.0 / (L + 2.0 * lambda2);
   const size_t smem = sizeof(double) * (size_t)(kReoptThreads / 32 + 2) * std::max(qmax, 1);
   if (smem > 48 * 1024) {
@@ -623,9 +653,10 @@ int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coe
                                                   d_scr, d_coef, d_obj);
   CKL("k_reopt");
   toc(KC_REOPT, 0.0);
-  if (tot) CK(cudaMemcpyAsync(coef, d_coef, sizeof(double) * tot, cudaMemcpyDeviceToHost, stream_));
-  CK(cudaMemcpyAsync(obj, d_obj, sizeof(double) * nsup, cudaMemcpyDeviceToHost, stream_));
+  if (tot) if (int rc_ = d2h(coef, d_coef, sizeof(double) * tot)) return rc_;
+  if (int rc_ = d2h(obj, d_obj, sizeof(double) * nsup)) return rc_;
   CK(cudaStreamSynchronize(stream_));
+  resolve_timing();
   return 0;
 }
 
@@ -637,15 +668,14 @@ int Engine::gemm_probe(int trans, int m, const double* Bh, double* Ch) {
     return rc;
   double* dBin = static_cast<double*>(dAux_);
   double* dC = dBin + (size_t)K * m;
-  CK(cudaMemcpyAsync(dBin, Bh, sizeof(double) * (size_t)K * m, cudaMemcpyHostToDevice, stream_));
-  CK(cudaMemcpyAsync(dMa_, &m, sizeof(int), cudaMemcpyHostToDevice, stream_));
+  if (int rc_ = h2d(dBin, Bh, sizeof(double) * (size_t)K * m)) return rc_;
+  if (int rc_ = h2d(dMa_, &m, sizeof(int))) return rc_;
   const GemmPlan pl = plan(Mo, K, m, trans != 0);
   if (int rc = launch_gemm(trans != 0, EPI_STORE, pl, dBin, K, dC, Mo, nullptr, dMa_,
                            (long long)Mo * m, m))
     return rc;
   std::vector<double> slabs((size_t)Mo * m * pl.nsplit);
-  CK(cudaMemcpyAsync(slabs.data(), dC, sizeof(double) * slabs.size(), cudaMemcpyDeviceToHost,
-                     stream_));
+  if (int rc_ = d2h(slabs.data(), dC, sizeof(double) * slabs.size())) return rc_;
   CK(cudaStreamSynchronize(stream_));
   for (size_t e = 0; e < (size_t)Mo * m; ++e) {
     double s = slabs[e];

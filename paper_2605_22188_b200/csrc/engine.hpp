@@ -72,6 +72,7 @@ class Engine {
   int n = 0, p = 0, k = 0, loss = 0, device = 0;
   double M = 1.0, lambda2 = 1.0, L = 0.0;
   long long launches = 0;
+  long long h2d_bytes = 0, d2h_bytes = 0;
   bool timing = false;
   double kc_ms[KC_COUNT] = {0};
   double kc_flops[KC_COUNT] = {0};
@@ -96,6 +97,17 @@ class Engine {
                   int part_ld);
   void tic(int kc);
   void toc(int kc, double flops);
+  void resolve_timing();
+  int h2d(void* dst, const void* src, size_t bytes);
+  int d2h(void* dst, const void* src, size_t bytes);
+  struct EvPair {
+    cudaEvent_t a, b;
+    int kc;
+  };
+  std::vector<EvPair> pending_;
+  std::vector<cudaEvent_t> ev_pool_;
+  cudaEvent_t cur_a_ = nullptr;
+  cudaEvent_t get_event();
 
   cudaStream_t stream_ = nullptr;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
