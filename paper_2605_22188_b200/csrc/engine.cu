@@ -231,13 +231,13 @@ void Engine::resolve_timing() {
 int Engine::h2d(void* dst, const void* src, size_t bytes) {
   if (!bytes) return 0;
   h2d_bytes += (long long)bytes;
-  if (int rc_ = h2d(dst, src, bytes)) return rc_;
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_));
   return 0;
 }
 int Engine::d2h(void* dst, const void* src, size_t bytes) {
   if (!bytes) return 0;
   d2h_bytes += (long long)bytes;
-  if (int rc_ = d2h(dst, src, bytes)) return rc_;
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream_));
   return 0;
 }
 
