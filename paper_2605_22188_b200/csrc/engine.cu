@@ -644,14 +644,28 @@ int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coe
   if (int rc_ = h2d(d_off, offsets, sizeof(int) * (nsup + 1))) return rc_;
   if (tot) if (int rc_ = h2d(d_idx, idx, sizeof(int) * tot)) return rc_;
   const double step = 1.0 / (L + 2.0 * lambda2);
-  const size_t smem = sizeof(double) * (size_t)(kReoptThreads / 32 + 2) * std::max(qmax, 1);
-  if (smem > 48 * 1024) {
-    CK(cudaFuncSetAttribute(k_reopt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  }
   tic(KC_REOPT);
-  k_reopt<<<nsup, kReoptThreads, smem, stream_>>>(n, dX_, dy_, loss, M, lambda2, step, d_off, d_idx,
-                                                  d_scr, d_coef, d_obj);
-  CKL("k_reopt");
+  if (loss == kSquared && qmax <= 32) {
+    k_reopt_gram<<<nsup, kReoptFastThreads, 0, stream_>>>(n, dX_, dy_, M, lambda2, step, d_off,
+                                                          d_idx, d_coef, d_obj);
+    CKL("k_reopt_gram");
+  } else if (qmax <= 8) {
+    k_reopt_direct<8><<<nsup, kReoptFastThreads, 0, stream_>>>(
+        n, dX_, dy_, loss, M, lambda2, step, d_off, d_idx, d_scr, d_coef, d_obj);
+    CKL("k_reopt_direct");
+  } else if (qmax <= 16) {
+    k_reopt_direct<16><<<nsup, kReoptFastThreads, 0, stream_>>>(
+        n, dX_, dy_, loss, M, lambda2, step, d_off, d_idx, d_scr, d_coef, d_obj);
+    CKL("k_reopt_direct");
+  } else {
+    const size_t smem = sizeof(double) * (size_t)(kReoptThreads / 32 + 2) * std::max(qmax, 1);
+    if (smem > 48 * 1024) {
+      CK(cudaFuncSetAttribute(k_reopt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    }
+    k_reopt<<<nsup, kReoptThreads, smem, stream_>>>(n, dX_, dy_, loss, M, lambda2, step, d_off,
+                                                    d_idx, d_scr, d_coef, d_obj);
+    CKL("k_reopt");
+  }
   toc(KC_REOPT, 0.0);
   if (tot) if (int rc_ = d2h(coef, d_coef, sizeof(double) * tot)) return rc_;
   if (int rc_ = d2h(obj, d_obj, sizeof(double) * nsup)) return rc_;

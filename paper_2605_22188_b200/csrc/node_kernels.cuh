@@ -111,54 +111,134 @@ __global__ void k_init_cols(int p, int m, const uint8_t* state, int* pf, const d
 }
 
 // --------------------------------------------------------------------------
-// Boundary-seeded PAVA on the sorted keys (prox_kernel.hpp:132-170), run by
-// one thread.  v_r = prox_huber(key_r, w, M) for r < kbar, key_r otherwise;
-// the pooled block [lo,hi] is re-summed in ascending rank order each time.
+// Block-wide inclusive scan of f(0..len-1) into out[] (each thread scans a
+// contiguous chunk, chunk totals are combined with a warp scan).  Fixed
+// association order, so the result is deterministic.
 // --------------------------------------------------------------------------
-__device__ __forceinline__ void pava_block(const double* key, int pf, int kbar, double w, double M,
-                                           int& blo, int& bhi, double& bval) {
+template <int NT, class F>
+__device__ __forceinline__ void block_scan_incl(int len, F f, double* out, double* wtot) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int chunk = (len + NT - 1) / NT;
+  const int beg = min(len, tid * chunk), end = min(len, beg + chunk);
+  double run = 0.0;
+  for (int i = beg; i < end; ++i) {
+    run += f(i);
+    out[i] = run;
+  }
+  double incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  __syncthreads();
+  if (lane == 31) wtot[warp] = incl;
+  __syncthreads();
+  double off = incl - run;
+  for (int w = 0; w < warp; ++w) off += wtot[w];
+  if (off != 0.0)
+    for (int i = beg; i < end; ++i) out[i] += off;
+  __syncthreads();
+}
+
+// --------------------------------------------------------------------------
+// Boundary-seeded PAVA on the sorted keys (prox_kernel.hpp:132-170).
+// v_r = prox_huber(key_r, w, M) for r < kbar and key_r otherwise; the only
+// violation is at the kbar boundary and the pooled block [lo,hi] grows from
+// [kbar-1, kbar] with the reference's rule (left first, then right).
+//
+// The reference re-sums the block after every expansion (O(len^2), one
+// thread).  Here the block sums come from two prefix scans anchored at the
+// boundary (left part SL, right part SR -- sums of block members only, so no
+// cancellation), and warp 0 evaluates 32 consecutive expansion states per
+// step, following the reference's decision sequence exactly: the first state
+// whose left test fires (or whose right test fails) is found with a ballot.
+// All threads call; lo/hi/pooled are returned to every thread.
+// --------------------------------------------------------------------------
+template <int NT>
+__device__ void block_pava(const double* key, int pf, int kbar, double w, double M, double* scan,
+                           double* wtot, int& blo, int& bhi, double& bval) {
+  __shared__ int s_lo, s_hi;
+  __shared__ double s_val;
   blo = 0;
   bhi = -1;
   bval = 0.0;
   if (kbar <= 0 || kbar >= pf) return;
   if (d_prox_huber(key[kbar - 1], w, M) >= key[kbar]) return;
-  int lo = kbar - 1, hi = kbar;
-  auto recompute = [&]() {
-    double sum = 0.0;
-    for (int r = lo; r <= hi; ++r) sum += key[r];
-    const int len = hi - lo + 1;
-    const double mean_w = w * (double)(kbar - lo) / len;
-    return d_prox_huber(sum / len, mean_w, M);
-  };
-  double pooled = recompute();
-  for (;;) {
-    if (lo > 0) {
-      const double vl = (lo - 1 < kbar) ? d_prox_huber(key[lo - 1], w, M) : key[lo - 1];
-      if (vl < pooled) {
-        --lo;
-        pooled = recompute();
-        continue;
-      }
-    }
-    if (hi < pf - 1) {
-      const double vr = (hi + 1 < kbar) ? d_prox_huber(key[hi + 1], w, M) : key[hi + 1];
-      if (pooled < vr) {
+  double* SL = scan;         // SL[i] = key[kbar-1] + ... + key[kbar-1-i]
+  double* SR = scan + kbar;  // SR[e] = key[kbar] + ... + key[kbar+e]
+  block_scan_incl<NT>(kbar, [&](int i) { return key[kbar - 1 - i]; }, SL, wtot);
+  block_scan_incl<NT>(pf - kbar, [&](int e) { return key[kbar + e]; }, SR, wtot);
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    auto pooled = [&](int lo, int hi) {
+      const int len = hi - lo + 1;
+      const double sum = SL[kbar - 1 - lo] + SR[hi - kbar];
+      const double mean_w = w * (double)(kbar - lo) / len;
+      return d_prox_huber(sum / len, mean_w, M);
+    };
+    auto v = [&](int r) { return r < kbar ? d_prox_huber(key[r], w, M) : key[r]; };
+    int lo = kbar - 1, hi = kbar;
+    bool left_phase = true;
+    for (;;) {
+      if (left_phase) {
+        // states (lo - lane, hi): L = left test, R = right test
+        const int cl = lo - lane;
+        bool L = false, R = false;
+        if (cl >= 0) {
+          const double pv = pooled(cl, hi);
+          L = cl > 0 && v(cl - 1) < pv;
+          R = hi < pf - 1 && pv < v(hi + 1);
+        }
+        const unsigned stop = __ballot_sync(0xffffffffu, !L);
+        if (!stop) {
+          lo -= 32;
+          continue;
+        }
+        const int i = __ffs(stop) - 1;
+        const bool Ri = __shfl_sync(0xffffffffu, R, i);
+        lo -= i;
+        if (!Ri) break;
         ++hi;
-        pooled = recompute();
-        continue;
+        left_phase = false;
+      } else {
+        // states (lo, hi + lane)
+        const int ch = hi + lane;
+        bool L = false, R = false;
+        if (ch <= pf - 1) {
+          const double pv = pooled(lo, ch);
+          L = lo > 0 && v(lo - 1) < pv;
+          R = ch < pf - 1 && pv < v(ch + 1);
+        }
+        const unsigned ev = __ballot_sync(0xffffffffu, L || !R);
+        if (!ev) {
+          hi += 32;
+          continue;
+        }
+        const int j = __ffs(ev) - 1;
+        const bool Lj = __shfl_sync(0xffffffffu, L, j);
+        hi += j;
+        if (!Lj) break;
+        --lo;
+        left_phase = true;
       }
     }
-    break;
+    if (lane == 0) {
+      s_lo = lo;
+      s_hi = hi;
+      s_val = pooled(lo, hi);
+    }
   }
-  blo = lo;
-  bhi = hi;
-  bval = pooled;
+  __syncthreads();
+  blo = s_lo;
+  bhi = s_hi;
+  bval = s_val;
 }
 
 // shared-memory layout of the column kernels: key[n2] doubles, idx[n2] ints,
-// u[p] doubles, red[8] doubles
+// u[p] doubles, scan[n2] doubles
 __host__ __device__ inline size_t column_smem_bytes(int p, int n2) {
-  return sizeof(double) * (size_t)n2 + sizeof(int) * (size_t)n2 + sizeof(double) * (size_t)p +
+  return sizeof(double) * (size_t)n2 * 2 + sizeof(int) * (size_t)n2 + sizeof(double) * (size_t)p +
          sizeof(double) * 16;
 }
 
@@ -174,8 +254,8 @@ __global__ void __launch_bounds__(kNodeThreads) k_prox_fista(RelaxDev r) {
   double* key = sm;
   int* idx = reinterpret_cast<int*>(key + n2);
   double* u = reinterpret_cast<double*>(idx + n2);
-  __shared__ int s_lohi[2];
-  __shared__ double s_pool;
+  double* scan = u + p;
+  __shared__ double wtot[kNodeThreads / 32];
 
   const uint8_t* st = r.state + (size_t)b * p;
   double* Vb = r.V + (size_t)b * p;
@@ -197,17 +277,9 @@ __global__ void __launch_bounds__(kNodeThreads) k_prox_fista(RelaxDev r) {
   if (bad) atomicMin(r.d_err, b);  // refresh_predictions' finite check (relaxation.hpp:76-81)
   bitonic_sort_desc<kNodeThreads>(key, idx, n2);
   const int kb = r.kbar[b], pf = r.pf[b];
-  if (threadIdx.x == 0) {
-    int lo, hi;
-    double pooled;
-    pava_block(key, pf, kb, r.rho, r.M, lo, hi, pooled);
-    s_lohi[0] = lo;
-    s_lohi[1] = hi;
-    s_pool = pooled;
-  }
-  __syncthreads();
-  const int lo = s_lohi[0], hi = s_lohi[1];
-  const double pooled = s_pool;
+  int lo, hi;
+  double pooled;
+  block_pava<kNodeThreads>(key, pf, kb, r.rho, r.M, scan, wtot, lo, hi, pooled);
   const double inv_rho = 1.0 / r.rho;
   const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * tm * tm));
   const double coef = (tm - 1.0) / t_next;
@@ -610,6 +682,209 @@ __global__ void __launch_bounds__(kReoptThreads)
 }
 
 // --------------------------------------------------------------------------
+// VK10 fast paths (q <= QMAX).  Every thread of the CTA keeps the whole
+// coefficient vector in registers and recomputes the update redundantly from
+// the same shared partial sums, so one barrier per iteration suffices and all
+// threads take the same stopping decision.
+//
+// k_reopt_direct: the reference's gather form (primal_heuristics.hpp:194-215):
+//   scores = sum_r beta_r X[:,S_r] (r ascending), deriv = l'(scores),
+//   grad_r = X[:,S_r]' deriv + 2 lambda2 beta_r, next = clip(beta - step grad).
+// --------------------------------------------------------------------------
+constexpr int kReoptFastThreads = 512;
+
+template <int QMAX>
+__global__ void __launch_bounds__(kReoptFastThreads)
+    k_reopt_direct(int n, const double* __restrict__ X, const double* __restrict__ y, int loss,
+                   double M, double lambda2, double step, const int* off, const int* sidx,
+                   double* deriv_scratch, double* coef_out, double* obj_out) {
+  constexpr int NW = kReoptFastThreads / 32;
+  __shared__ double red[2][NW][QMAX];
+  __shared__ const double* cols[QMAX];
+  __shared__ double wred[NW];
+  const int s = blockIdx.x;
+  const int q = off[s + 1] - off[s];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < q) cols[tid] = X + (size_t)sidx[off[s] + tid] * n;
+  __syncthreads();
+  double* d = deriv_scratch + (size_t)s * n;
+  double beta[QMAX];
+#pragma unroll
+  for (int r = 0; r < QMAX; ++r) beta[r] = 0.0;
+  int buf = 0;
+  if (q > 0) {
+    for (int it = 0; it < 5000; ++it) {
+      double part[QMAX];
+#pragma unroll
+      for (int r = 0; r < QMAX; ++r) part[r] = 0.0;
+      for (int i = tid; i < n; i += kReoptFastThreads) {
+        double sc = 0.0;
+#pragma unroll
+        for (int r = 0; r < QMAX; ++r)
+          if (r < q) sc += beta[r] * cols[r][i];
+        const double di = d_loss_deriv(loss, sc, y[i]);
+#pragma unroll
+        for (int r = 0; r < QMAX; ++r)
+          if (r < q) part[r] += cols[r][i] * di;
+      }
+#pragma unroll
+      for (int r = 0; r < QMAX; ++r) {
+        if (r < q) {
+          double a = part[r];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+          if (lane == 0) red[buf][warp][r] = a;
+        }
+      }
+      __syncthreads();
+      double gm2 = 0.0;
+#pragma unroll
+      for (int r = 0; r < QMAX; ++r) {
+        if (r < q) {
+          double g = 0.0;
+          for (int w = 0; w < NW; ++w) g += red[buf][w][r];
+          g += 2.0 * lambda2 * beta[r];
+          double v = beta[r] - step * g;
+          v = v < -M ? -M : v;
+          v = v > M ? M : v;
+          const double dl = beta[r] - v;
+          gm2 += dl * dl;
+          beta[r] = v;
+        }
+      }
+      buf ^= 1;
+      if (sqrt(gm2) / step <= 1e-8) break;
+    }
+  }
+  (void)d;
+  double acc = 0.0;
+  for (int i = tid; i < n; i += kReoptFastThreads) {
+    double sc = 0.0;
+#pragma unroll
+    for (int r = 0; r < QMAX; ++r)
+      if (r < q) sc += beta[r] * cols[r][i];
+    acc += d_loss_value(loss, sc, y[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) wred[warp] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double sq = 0.0;
+#pragma unroll
+    for (int r = 0; r < QMAX; ++r)
+      if (r < q) sq += beta[r] * beta[r];
+    double obj = lambda2 * sq;
+    for (int w = 0; w < NW; ++w) obj += wred[w];
+    obj_out[s] = obj;
+#pragma unroll
+    for (int r = 0; r < QMAX; ++r)
+      if (r < q) coef_out[off[s] + r] = beta[r];
+  }
+}
+
+// k_reopt_gram (squared loss): X_S'(X_S beta - y) = Gram beta - X_S'y, the
+// same iterates in exact arithmetic.  The q x q Gram and
+// X_S'y are built once per support; warp 0 then runs the projected-gradient
+// loop with lane r owning beta_r.  q <= 32.
+__global__ void __launch_bounds__(kReoptFastThreads)
+    k_reopt_gram(int n, const double* __restrict__ X, const double* __restrict__ y, double M,
+                 double lambda2, double step, const int* off, const int* sidx, double* coef_out,
+                 double* obj_out) {
+  constexpr int NW = kReoptFastThreads / 32;
+  __shared__ double gram[32][33];
+  __shared__ double xty[32];
+  __shared__ double bsh[32];
+  __shared__ double wred[NW];
+  __shared__ const double* cols[32];
+  const int s = blockIdx.x;
+  const int q = off[s + 1] - off[s];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < q) cols[tid] = X + (size_t)sidx[off[s] + tid] * n;
+  if (tid < 32) bsh[tid] = 0.0;
+  __syncthreads();
+  // Gram entries (r <= c) and X_S'y: one warp per dot product
+  const int npairs = q * (q + 1) / 2 + q;
+  for (int t = warp; t < npairs; t += NW) {
+    int r = 0, c = 0;
+    const double* a;
+    const double* bvec;
+    if (t < q * (q + 1) / 2) {
+      int tt = t;
+      while (tt >= q - r) {
+        tt -= q - r;
+        ++r;
+      }
+      c = r + tt;
+      a = cols[r];
+      bvec = cols[c];
+    } else {
+      r = t - q * (q + 1) / 2;
+      a = cols[r];
+      bvec = y;
+    }
+    double acc = 0.0;
+    for (int i = lane; i < n; i += 32) acc += a[i] * bvec[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      if (t < q * (q + 1) / 2) {
+        gram[r][c] = acc;
+        gram[c][r] = acc;
+      } else {
+        xty[r] = acc;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 0 && q > 0) {
+    double b = 0.0;
+    const bool own = lane < q;
+    for (int it = 0; it < 5000; ++it) {
+      double g = 0.0;
+      for (int c = 0; c < q; ++c) {
+        const double bc = __shfl_sync(0xffffffffu, b, c);
+        if (own) g += gram[lane][c] * bc;
+      }
+      double dl2 = 0.0, nx = 0.0;
+      if (own) {
+        g = g - xty[lane] + 2.0 * lambda2 * b;
+        double v = b - step * g;
+        v = v < -M ? -M : v;
+        v = v > M ? M : v;
+        nx = v;
+        const double dl = b - v;
+        dl2 = dl * dl;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dl2 += __shfl_xor_sync(0xffffffffu, dl2, o);
+      b = nx;
+      if (sqrt(dl2) / step <= 1e-8) break;
+    }
+    if (own) bsh[lane] = b;
+  }
+  __syncthreads();
+  double acc = 0.0;
+  for (int i = tid; i < n; i += kReoptFastThreads) {
+    double sc = 0.0;
+    for (int r = 0; r < q; ++r) sc += bsh[r] * cols[r][i];
+    acc += d_loss_value(kSquared, sc, y[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) wred[warp] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double sq = 0.0;
+    for (int r = 0; r < q; ++r) sq += bsh[r] * bsh[r];
+    double obj = lambda2 * sq;
+    for (int w = 0; w < NW; ++w) obj += wred[w];
+    obj_out[s] = obj;
+  }
+  if (tid < q) coef_out[off[s] + tid] = bsh[tid];
+}
+
+// --------------------------------------------------------------------------
 // stateless test kernels (prox_kernel.hpp:177-229, :284-301, :310-370)
 // --------------------------------------------------------------------------
 // mode 0: prox_step (out = U - rho^-1 prox_{rho g*}(rho U)); mode 1: conjugate prox
@@ -620,8 +895,7 @@ __global__ void __launch_bounds__(kNodeThreads)
   const int b = blockIdx.x;
   double* key = sm;
   int* idx = reinterpret_cast<int*>(key + n2);
-  __shared__ int s_lohi[2];
-  __shared__ double s_pool;
+  double* scan = reinterpret_cast<double*>(idx + n2);
   __shared__ double red[kNodeThreads / 32];
   const double* u = U + (size_t)b * p;
   const uint8_t* st = state + (size_t)b * p;
@@ -641,17 +915,9 @@ __global__ void __launch_bounds__(kNodeThreads)
   const int pf = (int)block_sum<kNodeThreads>((double)cnt, red);
   bitonic_sort_desc<kNodeThreads>(key, idx, n2);
   const int kb = kbar[b];
-  if (threadIdx.x == 0) {
-    int lo, hi;
-    double pooled;
-    pava_block(key, pf, kb, w, M, lo, hi, pooled);
-    s_lohi[0] = lo;
-    s_lohi[1] = hi;
-    s_pool = pooled;
-  }
-  __syncthreads();
-  const int lo = s_lohi[0], hi = s_lohi[1];
-  const double pooled = s_pool;
+  int lo, hi;
+  double pooled;
+  block_pava<kNodeThreads>(key, pf, kb, w, M, scan, red, lo, hi, pooled);
   for (int rk = threadIdx.x; rk < pf; rk += kNodeThreads) {
     const int j = idx[rk];
     const bool in_block = hi >= lo && rk >= lo && rk <= hi;
