@@ -289,17 +289,24 @@ def main():
     roof["kernel_ms"] = {kc: round(v[0], 3) for kc, v in delta.items()}
 
     # e2e: the public API from host arrays (instance upload, solve, certificate readback)
-    eng_h2d0, eng_d2h0 = 0, 0
     e2e_ms, e2e_nodes, h2d, d2h = 0.0, 0, 0, 0
+    e2e_parts = [0.0, 0.0, 0.0]  # create (upload + L), solve, destroy
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        with P.Engine(inst, device=local) as e2:
-            c2 = e2.solve(cfg)
-            bi, bo = e2.transfer_bytes()
+        e2 = P.Engine(inst, device=local)
+        t1 = time.perf_counter()
+        c2 = e2.solve(cfg)
+        bi, bo = e2.transfer_bytes()
+        t2 = time.perf_counter()
+        e2.close()
         torch.cuda.synchronize()
-        e2e_ms += 1e3 * (time.perf_counter() - t0)
+        t3 = time.perf_counter()
+        e2e_parts[0] += t1 - t0
+        e2e_parts[1] += t2 - t1
+        e2e_parts[2] += t3 - t2
+        e2e_ms += 1e3 * (t3 - t0)
         e2e_nodes += c2.nodes_processed
         h2d += bi
         d2h += bo + 8 * (2 * len(c2.support) + 16)
@@ -340,7 +347,8 @@ def main():
             "roofline": roof,
             "e2e": {"value": e2e_value, "unit": "nodes/s",
                     "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
-                    "time_to_certify_s": e2e_ms / args.steps / 1e3},
+                    "time_to_certify_s": e2e_ms / args.steps / 1e3,
+                    "create_solve_destroy_s": [round(x / args.steps, 5) for x in e2e_parts]},
             "cpu_baseline": base,
         }
         print(json.dumps(line), flush=True)

@@ -44,9 +44,18 @@ struct RelaxDev {
   int accel;
 };
 
+constexpr int kMaxSplit = 8;
+
+// G = sum of the split-K slabs, added in slab order (loads issued together)
 __device__ __forceinline__ double gsum(const RelaxDev& r, int b, int j) {
-  double g = r.G[(size_t)b * r.p + j];
-  for (int s = 1; s < r.nsplit; ++s) g += r.G[(size_t)s * r.split_stride + (size_t)b * r.p + j];
+  double part[kMaxSplit];
+#pragma unroll
+  for (int s = 0; s < kMaxSplit; ++s)
+    part[s] = s < r.nsplit ? r.G[(size_t)s * r.split_stride + (size_t)b * r.p + j] : 0.0;
+  double g = part[0];
+#pragma unroll
+  for (int s = 1; s < kMaxSplit; ++s)
+    if (s < r.nsplit) g += part[s];
   return g;
 }
 
@@ -158,8 +167,6 @@ __device__ __forceinline__ void block_scan_incl(int len, F f, double* out, doubl
 template <int NT>
 __device__ void block_pava(const double* key, int pf, int kbar, double w, double M, double* scan,
                            double* wtot, int& blo, int& bhi, double& bval) {
-  __shared__ int s_lo, s_hi;
-  __shared__ double s_val;
   blo = 0;
   bhi = -1;
   bval = 0.0;
@@ -169,70 +176,73 @@ __device__ void block_pava(const double* key, int pf, int kbar, double w, double
   double* SR = scan + kbar;  // SR[e] = key[kbar] + ... + key[kbar+e]
   block_scan_incl<NT>(kbar, [&](int i) { return key[kbar - 1 - i]; }, SL, wtot);
   block_scan_incl<NT>(pf - kbar, [&](int e) { return key[kbar + e]; }, SR, wtot);
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    auto pooled = [&](int lo, int hi) {
-      const int len = hi - lo + 1;
-      const double sum = SL[kbar - 1 - lo] + SR[hi - kbar];
-      const double mean_w = w * (double)(kbar - lo) / len;
-      return d_prox_huber(sum / len, mean_w, M);
-    };
-    auto v = [&](int r) { return r < kbar ? d_prox_huber(key[r], w, M) : key[r]; };
-    int lo = kbar - 1, hi = kbar;
-    bool left_phase = true;
-    for (;;) {
-      if (left_phase) {
-        // states (lo - lane, hi): L = left test, R = right test
-        const int cl = lo - lane;
-        bool L = false, R = false;
-        if (cl >= 0) {
-          const double pv = pooled(cl, hi);
-          L = cl > 0 && v(cl - 1) < pv;
-          R = hi < pf - 1 && pv < v(hi + 1);
-        }
-        const unsigned stop = __ballot_sync(0xffffffffu, !L);
-        if (!stop) {
-          lo -= 32;
-          continue;
-        }
-        const int i = __ffs(stop) - 1;
-        const bool Ri = __shfl_sync(0xffffffffu, R, i);
-        lo -= i;
-        if (!Ri) break;
-        ++hi;
-        left_phase = false;
-      } else {
-        // states (lo, hi + lane)
-        const int ch = hi + lane;
-        bool L = false, R = false;
-        if (ch <= pf - 1) {
-          const double pv = pooled(lo, ch);
-          L = lo > 0 && v(lo - 1) < pv;
-          R = ch < pf - 1 && pv < v(ch + 1);
-        }
-        const unsigned ev = __ballot_sync(0xffffffffu, L || !R);
-        if (!ev) {
-          hi += 32;
-          continue;
-        }
-        const int j = __ffs(ev) - 1;
-        const bool Lj = __shfl_sync(0xffffffffu, L, j);
-        hi += j;
-        if (!Lj) break;
-        --lo;
-        left_phase = true;
+  auto pooled = [&](int lo, int hi) {
+    const int len = hi - lo + 1;
+    const double sum = SL[kbar - 1 - lo] + SR[hi - kbar];
+    const double mean_w = w * (double)(kbar - lo) / len;
+    return d_prox_huber(sum / len, mean_w, M);
+  };
+  auto v = [&](int r) { return r < kbar ? d_prox_huber(key[r], w, M) : key[r]; };
+  // Each batch evaluates NT consecutive states of the current phase (thread
+  // t owns state t); the first event is found with a ballot + per-warp min.
+  // Shared scratch is double-buffered so one barrier per batch suffices.
+  __shared__ int s_first[2][NT / 32];
+  __shared__ unsigned char s_L[2][NT], s_R[2][NT];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int lo = kbar - 1, hi = kbar, buf = 0;
+  bool left_phase = true;
+  for (;;) {
+    bool L = false, R = false, ev;
+    if (left_phase) {  // state t = (lo - t, hi)
+      const int cl = lo - tid;
+      if (cl >= 0) {
+        const double pv = pooled(cl, hi);
+        L = cl > 0 && v(cl - 1) < pv;
+        R = hi < pf - 1 && pv < v(hi + 1);
       }
+      ev = !L;
+    } else {  // state t = (lo, hi + t)
+      const int ch = hi + tid;
+      if (ch <= pf - 1) {
+        const double pv = pooled(lo, ch);
+        L = lo > 0 && v(lo - 1) < pv;
+        R = ch < pf - 1 && pv < v(ch + 1);
+      }
+      ev = L || !R;
     }
-    if (lane == 0) {
-      s_lo = lo;
-      s_hi = hi;
-      s_val = pooled(lo, hi);
+    s_L[buf][tid] = L;
+    s_R[buf][tid] = R;
+    const unsigned bal = __ballot_sync(0xffffffffu, ev);
+    if (lane == 0) s_first[buf][warp] = bal ? warp * 32 + __ffs(bal) - 1 : NT;
+    __syncthreads();
+    int first = NT;
+#pragma unroll
+    for (int w2 = 0; w2 < NT / 32; ++w2) first = min(first, s_first[buf][w2]);
+    if (first == NT) {
+      if (left_phase)
+        lo -= NT;
+      else
+        hi += NT;
+      buf ^= 1;
+      continue;
+    }
+    const bool Lf = s_L[buf][first], Rf = s_R[buf][first];
+    buf ^= 1;
+    if (left_phase) {
+      lo -= first;
+      if (!Rf) break;
+      ++hi;
+      left_phase = false;
+    } else {
+      hi += first;
+      if (!Lf) break;
+      --lo;
+      left_phase = true;
     }
   }
-  __syncthreads();
-  blo = s_lo;
-  bhi = s_hi;
-  bval = s_val;
+  blo = lo;
+  bhi = hi;
+  bval = pooled(lo, hi);
 }
 
 // shared-memory layout of the column kernels: key[n2] doubles, idx[n2] ints,
