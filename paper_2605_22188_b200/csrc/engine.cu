@@ -7,6 +7,7 @@
 #include "engine.hpp"
 #include "gemm.cuh"
 #include "node_kernels.cuh"
+#include "reopt_kernels.cuh"
 #include "rng.hpp"
 
 namespace bnbg {
@@ -28,6 +29,53 @@ static int next_pow2(int v) {
   int r = 1;
   while (r < v) r <<= 1;
   return r;
+}
+
+// Elements per thread of the register column sort (0: shared-memory network).
+static int column_E(int n2) {
+  return n2 <= 256 ? 1 : n2 <= 512 ? 2 : n2 <= 1024 ? 4 : n2 <= 2048 ? 8 : 0;
+}
+
+#define DISPATCH_E(E_, ...)                   \
+  switch (E_) {                               \
+    case 1: {                                 \
+      constexpr int EV = 1;                   \
+      __VA_ARGS__;                            \
+    } break;                                  \
+    case 2: {                                 \
+      constexpr int EV = 2;                   \
+      __VA_ARGS__;                            \
+    } break;                                  \
+    case 4: {                                 \
+      constexpr int EV = 4;                   \
+      __VA_ARGS__;                            \
+    } break;                                  \
+    case 8: {                                 \
+      constexpr int EV = 8;                   \
+      __VA_ARGS__;                            \
+    } break;                                  \
+    default: {                                \
+      constexpr int EV = 0;                   \
+      __VA_ARGS__;                            \
+    } break;                                  \
+  }
+
+template <int E>
+static cudaError_t set_column_attrs(size_t smem) {
+  cudaError_t e = cudaFuncSetAttribute(k_prox_fista<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_eval<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_round_select<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_prox_standalone<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_g_standalone<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+  return e;
 }
 
 Engine::~Engine() {
@@ -115,14 +163,14 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
   CK(cudaMalloc(&dErr_, sizeof(int)));
   CK(set_all_smem_attrs());
   n2_ = next_pow2(std::max(p, 2));
-  const size_t csmem = column_smem_bytes(p, n2_);
-  if (csmem > 200 * 1024) return fail(1, "p too large for the column kernels");
-  CK(cudaFuncSetAttribute(k_prox_fista, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
-  CK(cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
-  CK(cudaFuncSetAttribute(k_round_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
-  CK(cudaFuncSetAttribute(k_prox_standalone, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)csmem));
-  CK(cudaFuncSetAttribute(k_g_standalone, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+  colE_ = column_E(n2_);
+  csmem_ = column_smem_bytes(p, n2_, colE_);
+  if (csmem_ > 220 * 1024) return fail(1, "p too large for the column kernels");
+  {
+    cudaError_t ea = cudaSuccess;
+    DISPATCH_E(colE_, ea = set_column_attrs<EV>(csmem_));
+    CK(ea);
+  }
   nrb_max_ = (n + 15) / 16;
   CK(cudaStreamSynchronize(stream_));
   if (L_ > 0.0) {
@@ -414,7 +462,7 @@ int Engine::step(int ma, double eta, double rho, const RelaxParams& cfg) {
   r.lambda2 = lambda2;
   r.accel = cfg.acceleration;
   tic(KC_PROX);
-  k_prox_fista<<<ma, kNodeThreads, column_smem_bytes(p, n2_), stream_>>>(r);
+  DISPATCH_E(colE_, k_prox_fista<EV><<<ma, kNodeThreads, csmem_, stream_>>>(r));
   CKL("k_prox_fista");
   toc(KC_PROX, 0.0);
   return 0;
@@ -470,7 +518,7 @@ int Engine::evaluate(int ma, double eta, double rho, const RelaxParams& cfg, int
   e.trace = trace;
   e.eval_idx = eval_idx;
   tic(KC_EVAL);
-  k_eval<<<ma, kNodeThreads, column_smem_bytes(p, n2_), stream_>>>(r, e);
+  DISPATCH_E(colE_, k_eval<EV><<<ma, kNodeThreads, csmem_, stream_>>>(r, e));
   CKL("k_eval");
   k_compact<<<1, 1024, 0, stream_>>>(dAct_, dMa_, dFrozen_);
   CKL("k_compact");
@@ -528,8 +576,9 @@ int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_
   out.status.resize(m);
   out.iters.resize(m);
   if (round_select) {
-    k_round_select<<<m, kNodeThreads, column_smem_bytes(p, n2_), stream_>>>(
-        p, n2_, std::max(k, 1), dB_, dState_, dKbar_, d_one_off, d_one_idx, dSup_, dLen_, dJb_);
+    DISPATCH_E(colE_, k_round_select<EV><<<m, kNodeThreads, csmem_, stream_>>>(
+                          p, n2_, std::max(k, 1), dB_, dState_, dKbar_, d_one_off, d_one_idx,
+                          dSup_, dLen_, dJb_));
     CKL("k_round_select");
     out.sup.resize((size_t)m * std::max(k, 1));
     out.len.resize(m);
@@ -614,9 +663,9 @@ int Engine::round_select(int m, const double* beta, const uint8_t* state, const 
     if (no)
       if (int rc_ = h2d(d_idx, one_idx, sizeof(int) * no)) return rc_;
   }
-  k_round_select<<<m, kNodeThreads, column_smem_bytes(p, n2_), stream_>>>(
-      p, n2_, std::max(k, 1), dB_, dState_, dKbar_, one_off ? d_off : nullptr,
-      one_off ? d_idx : nullptr, dSup_, dLen_, dJb_);
+  DISPATCH_E(colE_, k_round_select<EV><<<m, kNodeThreads, csmem_, stream_>>>(
+                        p, n2_, std::max(k, 1), dB_, dState_, dKbar_, one_off ? d_off : nullptr,
+                        one_off ? d_idx : nullptr, dSup_, dLen_, dJb_));
   CKL("k_round_select");
   if (sup)
     if (int rc_ = d2h(sup, dSup_, sizeof(int) * (size_t)m * std::max(k, 1))) return rc_;
@@ -732,7 +781,10 @@ int stateless_column_op(int device, int kind, int mode, int p, int m, const doub
   cudaError_t e = cudaSetDevice(device);
   DevScratch s;
   const int n2 = next_pow2(std::max(p, 2));
-  const size_t smem = column_smem_bytes(p, n2);
+  const int E = column_E(n2);
+  const size_t smem = column_smem_bytes(p, n2, E);
+  if (smem > 220 * 1024) return BNBG_INPUT_ERROR;
+  if (e == cudaSuccess) DISPATCH_E(E, e = set_column_attrs<EV>(smem));
   double* din = s.alloc<double>((size_t)p * m, e);
   uint8_t* dst = s.alloc<uint8_t>((size_t)p * m, e);
   int* dkb = s.alloc<int>(m, e);
@@ -742,17 +794,12 @@ int stateless_column_op(int device, int kind, int mode, int p, int m, const doub
   if (e == cudaSuccess) e = cudaMemcpy(dst, state, (size_t)p * m, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(dkb, kbar, sizeof(int) * m, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && kind == 0) {
-    e = cudaFuncSetAttribute(k_prox_standalone, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) {
-      k_prox_standalone<<<m, kNodeThreads, smem>>>(mode, p, n2, din, dst, dkb, w, M, dout);
-      e = cudaGetLastError();
-    }
+    DISPATCH_E(E, k_prox_standalone<EV><<<m, kNodeThreads, smem>>>(mode, p, n2, din, dst, dkb, w, M,
+                                                                   dout));
+    e = cudaGetLastError();
   } else if (e == cudaSuccess) {
-    e = cudaFuncSetAttribute(k_g_standalone, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) {
-      k_g_standalone<<<m, kNodeThreads, smem>>>(mode, p, n2, din, dst, dkb, M, dout);
-      e = cudaGetLastError();
-    }
+    DISPATCH_E(E, k_g_standalone<EV><<<m, kNodeThreads, smem>>>(mode, p, n2, din, dst, dkb, M, dout));
+    e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaMemcpy(out, dout, sizeof(double) * outn, cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) {

@@ -112,6 +112,8 @@ class Engine {
   cudaStream_t stream_ = nullptr;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   int n2_ = 1;
+  int colE_ = 0;        // elements per thread of the register column sort
+  size_t csmem_ = 0;    // dynamic shared memory of the column kernels
   int sms_ = 148;
   int mcap_ = 0;
   double* dX_ = nullptr;

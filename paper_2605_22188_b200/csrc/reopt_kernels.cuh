@@ -1,0 +1,352 @@
+// reopt_kernels.cuh -- VK10 re-optimisation and the smoothness-constant GEMVs.
+//
+//   k_reopt / k_reopt_direct / k_reopt_gram   reoptimize_supports
+//                                  (primal_heuristics.hpp:174-227)
+//   k_gemv_n / k_gemv_t / k_power_stats / k_scale   smoothness_constant
+//                                  power iteration (losses.hpp:86-112)
+#pragma once
+#include "device_math.cuh"
+
+namespace bnbg {
+
+// --------------------------------------------------------------------------
+// VK10: box-constrained refit of each support by projected gradient,
+// step 1/(L + 2 lambda2), stop at |beta - next|/step <= 1e-8 or 5000
+// iterations; objective exact at the returned coefficients.
+// --------------------------------------------------------------------------
+constexpr int kReoptThreads = 256;
+
+__global__ void __launch_bounds__(kReoptThreads)
+    k_reopt(int n, const double* __restrict__ X, const double* __restrict__ y, int loss, double M,
+            double lambda2, double step, const int* off, const int* sidx, double* deriv_scratch,
+            double* coef_out, double* obj_out) {
+  extern __shared__ __align__(16) double sm[];
+  constexpr int NW = kReoptThreads / 32;
+  const int s = blockIdx.x;
+  const int q = off[s + 1] - off[s];
+  const int* S = sidx + off[s];
+  double* beta = sm;            // q
+  double* red = beta + q;       // NW * q
+  double* nxt = red + NW * q;   // q
+  __shared__ int s_stop;
+  __shared__ double wred[NW];
+  double* d = deriv_scratch + (size_t)s * n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int r = tid; r < q; r += kReoptThreads) beta[r] = 0.0;
+  if (tid == 0) s_stop = 0;
+  __syncthreads();
+  if (q > 0) {
+    for (int it = 0; it < 5000; ++it) {
+      // scores and derivative for this thread's rows (primal_heuristics.hpp:194-209)
+      for (int i = tid; i < n; i += kReoptThreads) {
+        double sc = 0.0;
+        for (int r = 0; r < q; ++r) sc += beta[r] * X[(size_t)S[r] * n + i];
+        d[i] = d_loss_deriv(loss, sc, y[i]);
+      }
+      // grad_r = X_{S_r}' deriv (+ 2 lambda2 beta_r)  (:210-211)
+      for (int r = 0; r < q; ++r) {
+        const double* col = X + (size_t)S[r] * n;
+        double a = 0.0;
+        for (int i = tid; i < n; i += kReoptThreads) a += col[i] * d[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) red[warp * q + r] = a;
+      }
+      __syncthreads();
+      for (int r = tid; r < q; r += kReoptThreads) {
+        double gr = 0.0;
+        for (int w = 0; w < NW; ++w) gr += red[w * q + r];
+        gr += 2.0 * lambda2 * beta[r];
+        double v = beta[r] - step * gr;
+        v = v < -M ? -M : v;
+        v = v > M ? M : v;
+        nxt[r] = v;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double gm2 = 0.0;
+        for (int r = 0; r < q; ++r) {
+          const double dl = beta[r] - nxt[r];
+          gm2 += dl * dl;
+        }
+        s_stop = (sqrt(gm2) / step) <= 1e-8;
+      }
+      __syncthreads();
+      for (int r = tid; r < q; r += kReoptThreads) beta[r] = nxt[r];
+      const int stop = s_stop;
+      __syncthreads();
+      if (stop) break;
+    }
+  }
+  // objective lambda2 |beta|^2 + sum l(X_S beta)  (:217-222)
+  double acc = 0.0;
+  for (int i = tid; i < n; i += kReoptThreads) {
+    double sc = 0.0;
+    for (int r = 0; r < q; ++r) sc += beta[r] * X[(size_t)S[r] * n + i];
+    acc += d_loss_value(loss, sc, y[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) wred[warp] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double sq = 0.0;
+    for (int r = 0; r < q; ++r) sq += beta[r] * beta[r];
+    double obj = lambda2 * sq;
+    for (int w = 0; w < NW; ++w) obj += wred[w];
+    obj_out[s] = obj;
+  }
+  for (int r = tid; r < q; r += kReoptThreads) coef_out[off[s] + r] = beta[r];
+}
+
+// --------------------------------------------------------------------------
+// VK10 fast paths (q <= QMAX).  Every thread of the CTA keeps the whole
+// coefficient vector in registers and recomputes the update redundantly from
+// the same shared partial sums, so one barrier per iteration suffices and all
+// threads take the same stopping decision.
+//
+// k_reopt_direct: the reference's gather form (primal_heuristics.hpp:194-215):
+//   scores = sum_r beta_r X[:,S_r] (r ascending), deriv = l'(scores),
+//   grad_r = X[:,S_r]' deriv + 2 lambda2 beta_r, next = clip(beta - step grad).
+// --------------------------------------------------------------------------
+constexpr int kReoptFastThreads = 512;
+
+template <int QMAX>
+__global__ void __launch_bounds__(kReoptFastThreads)
+    k_reopt_direct(int n, const double* __restrict__ X, const double* __restrict__ y, int loss,
+                   double M, double lambda2, double step, const int* off, const int* sidx,
+                   double* deriv_scratch, double* coef_out, double* obj_out) {
+  constexpr int NW = kReoptFastThreads / 32;
+  __shared__ double red[2][NW][QMAX];
+  __shared__ const double* cols[QMAX];
+  __shared__ double wred[NW];
+  const int s = blockIdx.x;
+  const int q = off[s + 1] - off[s];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < q) cols[tid] = X + (size_t)sidx[off[s] + tid] * n;
+  __syncthreads();
+  double* d = deriv_scratch + (size_t)s * n;
+  double beta[QMAX];
+#pragma unroll
+  for (int r = 0; r < QMAX; ++r) beta[r] = 0.0;
+  int buf = 0;
+  if (q > 0) {
+    for (int it = 0; it < 5000; ++it) {
+      double part[QMAX];
+#pragma unroll
+      for (int r = 0; r < QMAX; ++r) part[r] = 0.0;
+      for (int i = tid; i < n; i += kReoptFastThreads) {
+        double sc = 0.0;
+#pragma unroll
+        for (int r = 0; r < QMAX; ++r)
+          if (r < q) sc += beta[r] * cols[r][i];
+        const double di = d_loss_deriv(loss, sc, y[i]);
+#pragma unroll
+        for (int r = 0; r < QMAX; ++r)
+          if (r < q) part[r] += cols[r][i] * di;
+      }
+#pragma unroll
+      for (int r = 0; r < QMAX; ++r) {
+        if (r < q) {
+          double a = part[r];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+          if (lane == 0) red[buf][warp][r] = a;
+        }
+      }
+      __syncthreads();
+      double gm2 = 0.0;
+#pragma unroll
+      for (int r = 0; r < QMAX; ++r) {
+        if (r < q) {
+          double g = 0.0;
+          for (int w = 0; w < NW; ++w) g += red[buf][w][r];
+          g += 2.0 * lambda2 * beta[r];
+          double v = beta[r] - step * g;
+          v = v < -M ? -M : v;
+          v = v > M ? M : v;
+          const double dl = beta[r] - v;
+          gm2 += dl * dl;
+          beta[r] = v;
+        }
+      }
+      buf ^= 1;
+      if (sqrt(gm2) / step <= 1e-8) break;
+    }
+  }
+  (void)d;
+  double acc = 0.0;
+  for (int i = tid; i < n; i += kReoptFastThreads) {
+    double sc = 0.0;
+#pragma unroll
+    for (int r = 0; r < QMAX; ++r)
+      if (r < q) sc += beta[r] * cols[r][i];
+    acc += d_loss_value(loss, sc, y[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) wred[warp] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double sq = 0.0;
+#pragma unroll
+    for (int r = 0; r < QMAX; ++r)
+      if (r < q) sq += beta[r] * beta[r];
+    double obj = lambda2 * sq;
+    for (int w = 0; w < NW; ++w) obj += wred[w];
+    obj_out[s] = obj;
+#pragma unroll
+    for (int r = 0; r < QMAX; ++r)
+      if (r < q) coef_out[off[s] + r] = beta[r];
+  }
+}
+
+// k_reopt_gram (squared loss): X_S'(X_S beta - y) = Gram beta - X_S'y, the
+// same iterates in exact arithmetic.  The q x q Gram and
+// X_S'y are built once per support; warp 0 then runs the projected-gradient
+// loop with lane r owning beta_r.  q <= 32.
+__global__ void __launch_bounds__(kReoptFastThreads)
+    k_reopt_gram(int n, const double* __restrict__ X, const double* __restrict__ y, double M,
+                 double lambda2, double step, const int* off, const int* sidx, double* coef_out,
+                 double* obj_out) {
+  constexpr int NW = kReoptFastThreads / 32;
+  __shared__ double gram[32][33];
+  __shared__ double xty[32];
+  __shared__ double bsh[32];
+  __shared__ double wred[NW];
+  __shared__ const double* cols[32];
+  const int s = blockIdx.x;
+  const int q = off[s + 1] - off[s];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < q) cols[tid] = X + (size_t)sidx[off[s] + tid] * n;
+  if (tid < 32) bsh[tid] = 0.0;
+  __syncthreads();
+  // Gram entries (r <= c) and X_S'y: one warp per dot product
+  const int npairs = q * (q + 1) / 2 + q;
+  for (int t = warp; t < npairs; t += NW) {
+    int r = 0, c = 0;
+    const double* a;
+    const double* bvec;
+    if (t < q * (q + 1) / 2) {
+      int tt = t;
+      while (tt >= q - r) {
+        tt -= q - r;
+        ++r;
+      }
+      c = r + tt;
+      a = cols[r];
+      bvec = cols[c];
+    } else {
+      r = t - q * (q + 1) / 2;
+      a = cols[r];
+      bvec = y;
+    }
+    double acc = 0.0;
+    for (int i = lane; i < n; i += 32) acc += a[i] * bvec[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      if (t < q * (q + 1) / 2) {
+        gram[r][c] = acc;
+        gram[c][r] = acc;
+      } else {
+        xty[r] = acc;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 0 && q > 0) {
+    double b = 0.0;
+    const bool own = lane < q;
+    for (int it = 0; it < 5000; ++it) {
+      double g = 0.0;
+      for (int c = 0; c < q; ++c) {
+        const double bc = __shfl_sync(0xffffffffu, b, c);
+        if (own) g += gram[lane][c] * bc;
+      }
+      double dl2 = 0.0, nx = 0.0;
+      if (own) {
+        g = g - xty[lane] + 2.0 * lambda2 * b;
+        double v = b - step * g;
+        v = v < -M ? -M : v;
+        v = v > M ? M : v;
+        nx = v;
+        const double dl = b - v;
+        dl2 = dl * dl;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dl2 += __shfl_xor_sync(0xffffffffu, dl2, o);
+      b = nx;
+      if (sqrt(dl2) / step <= 1e-8) break;
+    }
+    if (own) bsh[lane] = b;
+  }
+  __syncthreads();
+  double acc = 0.0;
+  for (int i = tid; i < n; i += kReoptFastThreads) {
+    double sc = 0.0;
+    for (int r = 0; r < q; ++r) sc += bsh[r] * cols[r][i];
+    acc += d_loss_value(kSquared, sc, y[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) wred[warp] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double sq = 0.0;
+    for (int r = 0; r < q; ++r) sq += bsh[r] * bsh[r];
+    double obj = lambda2 * sq;
+    for (int w = 0; w < NW; ++w) obj += wred[w];
+    obj_out[s] = obj;
+  }
+  if (tid < q) coef_out[off[s] + tid] = bsh[tid];
+}
+
+// --------------------------------------------------------------------------
+// smoothness constant (losses.hpp:86-112): power-iteration GEMVs
+// --------------------------------------------------------------------------
+__global__ void k_gemv_n(int n, int p, const double* __restrict__ X, const double* __restrict__ v,
+                         double* __restrict__ xv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int j = 0; j < p; ++j) s += X[(size_t)j * n + i] * v[j];
+  xv[i] = s;
+}
+
+__global__ void k_gemv_t(int n, int p, const double* __restrict__ X, const double* __restrict__ xv,
+                         double* __restrict__ w) {
+  const int j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= p) return;
+  const double* col = X + (size_t)j * n;
+  double s = 0.0;
+  for (int i = lane; i < n; i += 32) s += col[i] * xv[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) w[j] = s;
+}
+
+// out[0] = v.w, out[1] = |w|; single CTA of 256 threads
+__global__ void k_power_stats(int p, const double* v, const double* w, double* out) {
+  __shared__ double red[8];
+  double a = 0.0, c = 0.0;
+  for (int j = threadIdx.x; j < p; j += 256) {
+    a += v[j] * w[j];
+    c += w[j] * w[j];
+  }
+  const double dot = block_sum<256>(a, red);
+  const double nrm2 = block_sum<256>(c, red);
+  if (threadIdx.x == 0) {
+    out[0] = dot;
+    out[1] = sqrt(nrm2);
+  }
+}
+
+__global__ void k_scale(int p, const double* w, double wn, double* v) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < p) v[j] = w[j] / wn;
+}
+
+
+}  // namespace bnbg
