@@ -33,7 +33,7 @@ static int next_pow2(int v) {
 
 // Elements per thread of the register column sort (0: shared-memory network).
 static int column_E(int n2) {
-  return n2 <= 256 ? 1 : n2 <= 512 ? 2 : n2 <= 1024 ? 4 : n2 <= 2048 ? 8 : 0;
+  return n2 <= 256 ? 1 : n2 <= 512 ? 2 : n2 <= 1024 ? 4 : 0;
 }
 
 #define DISPATCH_E(E_, ...)                   \
@@ -48,10 +48,6 @@ static int column_E(int n2) {
     } break;                                  \
     case 4: {                                 \
       constexpr int EV = 4;                   \
-      __VA_ARGS__;                            \
-    } break;                                  \
-    case 8: {                                 \
-      constexpr int EV = 8;                   \
       __VA_ARGS__;                            \
     } break;                                  \
     default: {                                \

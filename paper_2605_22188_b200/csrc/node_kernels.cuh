@@ -21,6 +21,11 @@
 #pragma once
 #include "device_math.cuh"
 
+// Optional timing probe for the PAVA phases (tools/micro); empty in the product.
+#ifndef BNBG_PAVA_PROBE
+#define BNBG_PAVA_PROBE(i)
+#endif
+
 namespace bnbg {
 
 constexpr int kNodeThreads = 256;
@@ -225,6 +230,7 @@ __device__ void block_pava(const double* key, int pf, int kbar, double w, double
   bval = 0.0;
   if (kbar <= 0 || kbar >= pf) return;
   if (d_prox_huber(key[kbar - 1], w, M) >= key[kbar]) return;
+  BNBG_PAVA_PROBE(0);
   constexpr int NW = NT / 32;
   __shared__ double s_ftot[NW], s_btot[NW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -265,16 +271,40 @@ __device__ void block_pava(const double* key, int pf, int kbar, double w, double
         SL[kbar - 1 - r] = run;
       }
     __syncthreads();
+  BNBG_PAVA_PROBE(1);
   }
+  // Values are kept as fractions num/den (den > 0) so the expansion tests
+  // need no division: pooled(lo,hi) = prox_huber(S/len, w(kbar-lo)/len, M)
+  // = S/(len + W) inside the box (|S| <= (len + W) M, W = w (kbar-lo)) and
+  // (S - W M)/len outside (S >= 0: keys are magnitudes); head values
+  // v_r = prox_huber(key_r, w, M) likewise.  Only the final pooled value is
+  // divided out (prox_kernel.hpp:145-151 evaluates the same quantity).
+  struct Frac {
+    double num, den;
+  };
+  auto pooled_f = [&](int lo, int hi) {
+    const double len = (double)(hi - lo + 1);
+    const double S = SL[kbar - 1 - lo] + SR[hi - kbar];
+    const double W = w * (double)(kbar - lo);
+    if (S <= (len + W) * M) return Frac{S, len + W};
+    return Frac{S - W * M, len};
+  };
+  auto v_f = [&](int r) {
+    const double a = key[r];
+    if (r >= kbar) return Frac{a, 1.0};
+    if (a <= (1.0 + w) * M) return Frac{a, 1.0 + w};
+    return Frac{a - w * M, 1.0};
+  };
+  auto less = [](const Frac& x, const Frac& y) { return x.num * y.den < y.num * x.den; };
   auto pooled = [&](int lo, int hi) {
     const int len = hi - lo + 1;
     const double sum = SL[kbar - 1 - lo] + SR[hi - kbar];
     const double mean_w = w * (double)(kbar - lo) / len;
     return d_prox_huber(sum / len, mean_w, M);
   };
-  auto v = [&](int r) { return r < kbar ? d_prox_huber(key[r], w, M) : key[r]; };
   __shared__ int s_first[2][NW];
   __shared__ unsigned char s_L[2][NT], s_R[2][NT];
+  BNBG_PAVA_PROBE(2);
   int lo = kbar - 1, hi = kbar, buf = 0;
   bool left_phase = true;
   for (;;) {
@@ -282,17 +312,17 @@ __device__ void block_pava(const double* key, int pf, int kbar, double w, double
     if (left_phase) {  // state t = (lo - t, hi)
       const int cl = lo - tid;
       if (cl >= 0) {
-        const double pv = pooled(cl, hi);
-        L = cl > 0 && v(cl - 1) < pv;
-        R = hi < pf - 1 && pv < v(hi + 1);
+        const Frac pv = pooled_f(cl, hi);
+        L = cl > 0 && less(v_f(cl - 1), pv);
+        R = hi < pf - 1 && less(pv, v_f(hi + 1));
       }
       ev = !L;
     } else {  // state t = (lo, hi + t)
       const int ch = hi + tid;
       if (ch <= pf - 1) {
-        const double pv = pooled(lo, ch);
-        L = lo > 0 && v(lo - 1) < pv;
-        R = ch < pf - 1 && pv < v(ch + 1);
+        const Frac pv = pooled_f(lo, ch);
+        L = lo > 0 && less(v_f(lo - 1), pv);
+        R = ch < pf - 1 && less(pv, v_f(ch + 1));
       }
       ev = L || !R;
     }
@@ -328,7 +358,9 @@ __device__ void block_pava(const double* key, int pf, int kbar, double w, double
   }
   blo = lo;
   bhi = hi;
+  BNBG_PAVA_PROBE(3);
   bval = pooled(lo, hi);
+  BNBG_PAVA_PROBE(4);
 }
 
 // Column shared-memory carve-up used by every column kernel.
