@@ -268,13 +268,19 @@ def main():
     dom = max(delta, key=lambda kc: delta[kc][0])
     ms, fl, ln = delta[dom]
     peaks = _load_peaks()
-    if dom.startswith("gemm"):
+    algorithmic = {
+        "gemm_xv": "2*n*p flops per active column per launch",
+        "gemm_xtr": "2*n*p flops per active column per launch",
+        "pass": "4*n*p flops per node-iteration (X*V and X'*R; bound evaluations not counted)",
+        "reopt": "4*q*n flops per support-iteration of the reference's projected gradient",
+    }
+    if dom in algorithmic:
         achieved = fl / (ms / 1e3) / 1e12
         roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
                 "peak_source": "measured FP64 DMMA issue rate (profiles/r01_fp64_peak.txt); "
                                "MEASURED_PEAKS.json has no fp64 entry",
-                "algorithmic": "2*n*p flops per active column per launch"}
+                "algorithmic": algorithmic[dom]}
     else:
         node_its = prof_cert.node_iterations
         bytes_ = 41.0 * p * node_its if dom == "prox_fista" else float("nan")

@@ -356,7 +356,7 @@ class Engine:
     def set_timing(self, on: bool):
         _L.lib().bnbg_set_timing(self._h, int(on))
 
-    KERNEL_CLASSES = ("gemm_xv", "gemm_xtr", "prox_fista", "eval", "reopt")
+    KERNEL_CLASSES = ("gemm_xv", "gemm_xtr", "prox_fista", "eval", "reopt", "pass")
 
     def kernel_stats(self):
         """{class: (ms, flops, launches)} -- ms only while timing is enabled."""

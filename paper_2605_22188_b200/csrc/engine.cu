@@ -2,11 +2,13 @@
 // loop (relaxation.hpp:163-255), rounding/branch selection and re-opt.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine.hpp"
 #include "gemm.cuh"
 #include "node_kernels.cuh"
+#include "launchers.hpp"
 #include "reopt_kernels.cuh"
 #include "rng.hpp"
 
@@ -29,49 +31,6 @@ static int next_pow2(int v) {
   int r = 1;
   while (r < v) r <<= 1;
   return r;
-}
-
-// Elements per thread of the register column sort (0: shared-memory network).
-static int column_E(int n2) {
-  return n2 <= 256 ? 1 : n2 <= 512 ? 2 : n2 <= 1024 ? 4 : 0;
-}
-
-#define DISPATCH_E(E_, ...)                   \
-  switch (E_) {                               \
-    case 1: {                                 \
-      constexpr int EV = 1;                   \
-      __VA_ARGS__;                            \
-    } break;                                  \
-    case 2: {                                 \
-      constexpr int EV = 2;                   \
-      __VA_ARGS__;                            \
-    } break;                                  \
-    case 4: {                                 \
-      constexpr int EV = 4;                   \
-      __VA_ARGS__;                            \
-    } break;                                  \
-    default: {                                \
-      constexpr int EV = 0;                   \
-      __VA_ARGS__;                            \
-    } break;                                  \
-  }
-
-template <int E>
-static cudaError_t set_column_attrs(size_t smem) {
-  cudaError_t e = cudaFuncSetAttribute(k_prox_fista<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_eval<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_round_select<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_prox_standalone<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_g_standalone<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-  return e;
 }
 
 Engine::~Engine() {
@@ -99,6 +58,7 @@ Engine::~Engine() {
   cudaFree(dLen_);
   cudaFree(dJb_);
   cudaFree(dAux_);
+  cudaFree(dPassOut_);
   if (hPin_) cudaFreeHost(hPin_);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
@@ -113,27 +73,6 @@ int Engine::fail(int code, const std::string& msg) {
 int Engine::cuda_fail(cudaError_t e, const char* what) {
   err = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
   return 4;  // BNBG_CUDA_ERROR
-}
-
-template <bool TN, int FM, int FN, int EPI>
-static cudaError_t set_smem_attr() {
-  return cudaFuncSetAttribute(k_gemm<TN, FM, FN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)GemmShape<TN, FM, FN>::SMEM_BYTES);
-}
-
-#define FOR_GEMM_CFGS(X)                                                              \
-  X(2, 1) X(2, 2) X(2, 4) X(4, 1) X(4, 2) X(4, 4) X(8, 1) X(8, 2) X(8, 4)
-
-static cudaError_t set_all_smem_attrs() {
-  cudaError_t e = cudaSuccess;
-#define SETA(FM, FN)                                                 \
-  if (e == cudaSuccess) e = set_smem_attr<false, FM, FN, EPI_DERIV>(); \
-  if (e == cudaSuccess) e = set_smem_attr<false, FM, FN, EPI_EVAL>();  \
-  if (e == cudaSuccess) e = set_smem_attr<false, FM, FN, EPI_STORE>(); \
-  if (e == cudaSuccess) e = set_smem_attr<true, FM, FN, EPI_STORE>();
-  FOR_GEMM_CFGS(SETA)
-#undef SETA
-  return e;
 }
 
 int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, int k_, double M_,
@@ -157,15 +96,25 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
   if (int rc_ = h2d(dy_, y, sizeof(double) * (size_t)n)) return rc_;
   CK(cudaMalloc(&dMa_, sizeof(int)));
   CK(cudaMalloc(&dErr_, sizeof(int)));
-  CK(set_all_smem_attrs());
+  CK(gemm_set_attrs());
   n2_ = next_pow2(std::max(p, 2));
   colE_ = column_E(n2_);
   csmem_ = column_smem_bytes(p, n2_, colE_);
   if (csmem_ > 220 * 1024) return fail(1, "p too large for the column kernels");
+  CK(column_set_attrs(colE_, csmem_));
+  // persistent pass kernel: one CTA per SM when it fits (BNBG_PERSISTENT=0 disables)
   {
-    cudaError_t ea = cudaSuccess;
-    DISPATCH_E(colE_, ea = set_column_attrs<EV>(csmem_));
-    CK(ea);
+    const char* env = getenv("BNBG_PERSISTENT");
+    int coop = 0;
+    CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+    pass_smem_ = pass_smem(p, n2_, colE_);
+    pass_grid_ = 0;
+    if (coop && !(env && env[0] == '0') && pass_smem_ <= 220 * 1024) {
+      int nb = 0;
+      CK(pass_setup(colE_, pass_smem_, &nb));
+      if (nb >= 1) pass_grid_ = sms_;
+    }
+    CK(cudaMalloc(&dPassOut_, 4 * sizeof(long long)));
   }
   nrb_max_ = (n + 15) / 16;
   CK(cudaStreamSynchronize(stream_));
@@ -338,26 +287,8 @@ int Engine::launch_gemm(bool tn, int epi, const GemmPlan& pl, const double* Bsrc
   g.part_loss = dPL_;
   g.part_conj = dPC_;
   g.part_ld = part_ld;
-  const dim3 block(kGemmThreads);
-#define LAUNCH_ONE(FM, FN)                                                                    \
-  if (pl.fm == FM && pl.fn == FN) {                                                           \
-    if (tn) {                                                                                 \
-      k_gemm<true, FM, FN, EPI_STORE>                                                         \
-          <<<pl.grid, block, GemmShape<true, FM, FN>::SMEM_BYTES, stream_>>>(g);              \
-    } else if (epi == EPI_DERIV) {                                                            \
-      k_gemm<false, FM, FN, EPI_DERIV>                                                        \
-          <<<pl.grid, block, GemmShape<false, FM, FN>::SMEM_BYTES, stream_>>>(g);             \
-    } else if (epi == EPI_EVAL) {                                                             \
-      k_gemm<false, FM, FN, EPI_EVAL>                                                         \
-          <<<pl.grid, block, GemmShape<false, FM, FN>::SMEM_BYTES, stream_>>>(g);             \
-    } else {                                                                                  \
-      k_gemm<false, FM, FN, EPI_STORE>                                                        \
-          <<<pl.grid, block, GemmShape<false, FM, FN>::SMEM_BYTES, stream_>>>(g);             \
-    }                                                                                         \
-  }
-  FOR_GEMM_CFGS(LAUNCH_ONE)
-#undef LAUNCH_ONE
-  CKL("k_gemm");
+  ++launches;
+  CK(gemm_launch(tn, epi, pl.fm, pl.fn, pl.grid, stream_, g));
   return 0;
 }
 
@@ -458,8 +389,8 @@ int Engine::step(int ma, double eta, double rho, const RelaxParams& cfg) {
   r.lambda2 = lambda2;
   r.accel = cfg.acceleration;
   tic(KC_PROX);
-  DISPATCH_E(colE_, k_prox_fista<EV><<<ma, kNodeThreads, csmem_, stream_>>>(r));
-  CKL("k_prox_fista");
+  ++launches;
+  CK(launch_prox_fista(colE_, ma, csmem_, stream_, r));
   toc(KC_PROX, 0.0);
   return 0;
 }
@@ -514,8 +445,8 @@ int Engine::evaluate(int ma, double eta, double rho, const RelaxParams& cfg, int
   e.trace = trace;
   e.eval_idx = eval_idx;
   tic(KC_EVAL);
-  DISPATCH_E(colE_, k_eval<EV><<<ma, kNodeThreads, csmem_, stream_>>>(r, e));
-  CKL("k_eval");
+  ++launches;
+  CK(launch_eval(colE_, ma, csmem_, stream_, r, e));
   k_compact<<<1, 1024, 0, stream_>>>(dAct_, dMa_, dFrozen_);
   CKL("k_compact");
   toc(KC_EVAL, 0.0);
@@ -526,6 +457,93 @@ int Engine::evaluate(int ma, double eta, double rho, const RelaxParams& cfg, int
   if (hPin_[1] != 0x7fffffff) {
     return fail(2, "relaxation: non-finite iterate in column " + std::to_string(hPin_[1]));
   }
+  return 0;
+}
+
+// The relaxation of a narrow batch as one persistent cooperative kernel
+// (pass_kernel.cuh).  Same per-phase code as the multi-kernel path.
+int Engine::run_pass(int m, const RelaxParams& cfg, double thr, double eta, double rho,
+                     double* dTrace, int& iter, int& n_evals, long long& node_its) {
+  (void)m;
+  PassArgs a;
+  RelaxDev& r = a.r;
+  r.p = p;
+  r.n2 = n2_;
+  r.mcap = mcap_;
+  r.B = dB_;
+  r.V = dV_;
+  r.G = dG_;
+  r.split_stride = (long long)p * mcap_;
+  r.nsplit = 1;
+  r.state = dState_;
+  r.kbar = dKbar_;
+  r.pf = dPf_;
+  r.t = dT_;
+  r.best = dBest_;
+  r.last_gap = dLast_;
+  r.frozen = dFrozen_;
+  r.status = dStatus_;
+  r.iters = dIters_;
+  r.act = dAct_;
+  r.d_ma = dMa_;
+  r.d_err = dErr_;
+  r.eta = eta;
+  r.rho = rho;
+  r.M = M;
+  r.lambda2 = lambda2;
+  r.accel = cfg.acceleration;
+  GemmArgs& g1 = a.nn;
+  g1.M = n;
+  g1.K = p;
+  g1.A = dX_;
+  g1.lda = n;
+  g1.B = dV_;
+  g1.ldb = p;
+  g1.C = dR_;
+  g1.ldc = n;
+  g1.split_stride = 0;
+  g1.ksplit = ((p + kBK - 1) / kBK) * kBK;
+  g1.act = dAct_;
+  g1.d_ncols = dMa_;
+  g1.y = dy_;
+  g1.loss = loss;
+  g1.part_loss = dPL_;
+  g1.part_conj = dPC_;
+  g1.part_ld = mcap_;
+  GemmArgs& g2 = a.tn;
+  g2 = g1;
+  g2.M = p;
+  g2.K = n;
+  g2.B = dR_;
+  g2.ldb = n;
+  g2.C = dG_;
+  g2.ldc = p;
+  g2.split_stride = (long long)p * mcap_;
+  a.n = n;
+  a.p = p;
+  a.max_it = cfg.max_iterations;
+  a.check = cfg.check_interval;
+  a.gap_tol = cfg.gap_tolerance;
+  a.prune_thr = thr;
+  a.trace = dTrace;
+  a.out = dPassOut_;
+  tic(KC_PASS);
+  cudaError_t e = cudaSuccess;
+  e = pass_launch(colE_, pass_grid_, pass_smem_, stream_, &a);
+  ++launches;
+  CK(e);
+  long long h_out[4] = {0, 0, 0, 0};
+  if (int rc = d2h(h_out, dPassOut_, 3 * sizeof(long long))) return rc;
+  if (int rc = d2h(hPin_ + 1, dErr_, sizeof(int))) return rc;
+  CK(cudaStreamSynchronize(stream_));
+  iter = (int)h_out[0];
+  n_evals = (int)h_out[1];
+  node_its = h_out[2];
+  // algorithmic FP64 work: 4np per node-iteration (X V and X'R) -- evaluations excluded
+  toc(KC_PASS, 4.0 * n * p * (double)node_its);
+  resolve_timing();
+  if (hPin_[1] != 0x7fffffff)
+    return fail(2, "relaxation: non-finite iterate in column " + std::to_string(hPin_[1]));
   return 0;
 }
 
@@ -546,24 +564,29 @@ int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_
   int iter = 0, last_eval = 0, ma = m, n_evals = 0;
   long long node_its = 0;
   int rc = 0;
-  while (iter < cfg.max_iterations && ma > 0) {
-    const int to_check = cfg.check_interval - iter % cfg.check_interval;
-    const int nsteps = std::min(to_check, cfg.max_iterations - iter);
-    for (int s = 0; s < nsteps; ++s) {
-      if ((rc = step(ma, eta, rho, cfg))) goto done;
+  if (pass_grid_ > 0 && m <= 2 * sms_) {
+    // narrow batch: the whole relaxation as one persistent cooperative kernel
+    if ((rc = run_pass(m, cfg, thr, eta, rho, dTrace, iter, n_evals, node_its))) goto done;
+  } else {
+    while (iter < cfg.max_iterations && ma > 0) {
+      const int to_check = cfg.check_interval - iter % cfg.check_interval;
+      const int nsteps = std::min(to_check, cfg.max_iterations - iter);
+      for (int s = 0; s < nsteps; ++s) {
+        if ((rc = step(ma, eta, rho, cfg))) goto done;
+      }
+      node_its += (long long)nsteps * ma;
+      iter += nsteps;
+      if (iter % cfg.check_interval == 0) {
+        if ((rc = evaluate(ma, eta, rho, cfg, iter, thr, dTrace, n_evals))) goto done;
+        ++n_evals;
+        last_eval = iter;
+        ma = hPin_[0];
+      }
     }
-    node_its += (long long)nsteps * ma;
-    iter += nsteps;
-    if (iter % cfg.check_interval == 0) {
+    if (ma > 0 && last_eval != iter) {
       if ((rc = evaluate(ma, eta, rho, cfg, iter, thr, dTrace, n_evals))) goto done;
       ++n_evals;
-      last_eval = iter;
-      ma = hPin_[0];
     }
-  }
-  if (ma > 0 && last_eval != iter) {
-    if ((rc = evaluate(ma, eta, rho, cfg, iter, thr, dTrace, n_evals))) goto done;
-    ++n_evals;
   }
   out.iterations = iter;
   out.node_iterations = node_its;
@@ -572,10 +595,9 @@ int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_
   out.status.resize(m);
   out.iters.resize(m);
   if (round_select) {
-    DISPATCH_E(colE_, k_round_select<EV><<<m, kNodeThreads, csmem_, stream_>>>(
-                          p, n2_, std::max(k, 1), dB_, dState_, dKbar_, d_one_off, d_one_idx,
-                          dSup_, dLen_, dJb_));
-    CKL("k_round_select");
+    ++launches;
+    CK(launch_round_select(colE_, m, csmem_, stream_, p, n2_, std::max(k, 1), dB_, dState_, dKbar_,
+                           d_one_off, d_one_idx, dSup_, dLen_, dJb_));
     out.sup.resize((size_t)m * std::max(k, 1));
     out.len.resize(m);
     out.jbranch.resize(m);
@@ -659,10 +681,9 @@ int Engine::round_select(int m, const double* beta, const uint8_t* state, const 
     if (no)
       if (int rc_ = h2d(d_idx, one_idx, sizeof(int) * no)) return rc_;
   }
-  DISPATCH_E(colE_, k_round_select<EV><<<m, kNodeThreads, csmem_, stream_>>>(
-                        p, n2_, std::max(k, 1), dB_, dState_, dKbar_, one_off ? d_off : nullptr,
-                        one_off ? d_idx : nullptr, dSup_, dLen_, dJb_));
-  CKL("k_round_select");
+  ++launches;
+  CK(launch_round_select(colE_, m, csmem_, stream_, p, n2_, std::max(k, 1), dB_, dState_, dKbar_,
+                         one_off ? d_off : nullptr, one_off ? d_idx : nullptr, dSup_, dLen_, dJb_));
   if (sup)
     if (int rc_ = d2h(sup, dSup_, sizeof(int) * (size_t)m * std::max(k, 1))) return rc_;
   if (len) if (int rc_ = d2h(len, dLen_, sizeof(int) * m)) return rc_;
@@ -678,29 +699,34 @@ int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coe
   const int tot = offsets[nsup];
   int qmax = 0;
   for (int s = 0; s < nsup; ++s) qmax = std::max(qmax, offsets[s + 1] - offsets[s]);
-  const size_t bytes = sizeof(double) * ((size_t)nsup * n + tot + nsup + 2) +
-                       sizeof(int) * ((size_t)nsup + 1 + tot + 2);
+  const bool gram = loss == kSquared && qmax <= 32;
+  const bool direct = !gram && qmax <= 16;
+  // the deriv scratch is only used by the generic kernel
+  const size_t scr = (gram || direct) ? 0 : (size_t)nsup * n;
+  const size_t bytes = sizeof(double) * (scr + tot + nsup + 2) +
+                       sizeof(int) * ((size_t)2 * nsup + 1 + tot + 2);
   if (int rc = ensure_aux(bytes)) return rc;
   double* d_scr = static_cast<double*>(dAux_);
-  double* d_coef = d_scr + (size_t)nsup * n;
+  double* d_coef = d_scr + scr;
   double* d_obj = d_coef + tot + 1;
   int* d_off = reinterpret_cast<int*>(d_obj + nsup + 1);
   int* d_idx = d_off + nsup + 1;
+  int* d_its = d_idx + tot + 1;
   if (int rc_ = h2d(d_off, offsets, sizeof(int) * (nsup + 1))) return rc_;
   if (tot) if (int rc_ = h2d(d_idx, idx, sizeof(int) * tot)) return rc_;
   const double step = 1.0 / (L + 2.0 * lambda2);
   tic(KC_REOPT);
-  if (loss == kSquared && qmax <= 32) {
+  if (gram) {
     k_reopt_gram<<<nsup, kReoptFastThreads, 0, stream_>>>(n, dX_, dy_, M, lambda2, step, d_off,
-                                                          d_idx, d_coef, d_obj);
+                                                          d_idx, d_coef, d_obj, d_its);
     CKL("k_reopt_gram");
   } else if (qmax <= 8) {
     k_reopt_direct<8><<<nsup, kReoptFastThreads, 0, stream_>>>(
-        n, dX_, dy_, loss, M, lambda2, step, d_off, d_idx, d_scr, d_coef, d_obj);
+        n, dX_, dy_, loss, M, lambda2, step, d_off, d_idx, d_scr, d_coef, d_obj, d_its);
     CKL("k_reopt_direct");
   } else if (qmax <= 16) {
     k_reopt_direct<16><<<nsup, kReoptFastThreads, 0, stream_>>>(
-        n, dX_, dy_, loss, M, lambda2, step, d_off, d_idx, d_scr, d_coef, d_obj);
+        n, dX_, dy_, loss, M, lambda2, step, d_off, d_idx, d_scr, d_coef, d_obj, d_its);
     CKL("k_reopt_direct");
   } else {
     const size_t smem = sizeof(double) * (size_t)(kReoptThreads / 32 + 2) * std::max(qmax, 1);
@@ -708,13 +734,21 @@ int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coe
       CK(cudaFuncSetAttribute(k_reopt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
     k_reopt<<<nsup, kReoptThreads, smem, stream_>>>(n, dX_, dy_, loss, M, lambda2, step, d_off,
-                                                    d_idx, d_scr, d_coef, d_obj);
+                                                    d_idx, d_scr, d_coef, d_obj, d_its);
     CKL("k_reopt");
   }
-  toc(KC_REOPT, 0.0);
+  std::vector<int> its(nsup);
   if (tot) if (int rc_ = d2h(coef, d_coef, sizeof(double) * tot)) return rc_;
   if (int rc_ = d2h(obj, d_obj, sizeof(double) * nsup)) return rc_;
+  if (int rc_ = d2h(its.data(), d_its, sizeof(int) * nsup)) return rc_;
   CK(cudaStreamSynchronize(stream_));
+  // algorithmic work of the reference iteration: 4 q n flops per support-iteration
+  double flops = 0.0;
+  for (int s = 0; s < nsup; ++s) {
+    flops += 4.0 * (offsets[s + 1] - offsets[s]) * (double)n * its[s];
+    reopt_iterations += its[s];
+  }
+  toc(KC_REOPT, flops);
   resolve_timing();
   return 0;
 }
@@ -780,7 +814,7 @@ int stateless_column_op(int device, int kind, int mode, int p, int m, const doub
   const int E = column_E(n2);
   const size_t smem = column_smem_bytes(p, n2, E);
   if (smem > 220 * 1024) return BNBG_INPUT_ERROR;
-  if (e == cudaSuccess) DISPATCH_E(E, e = set_column_attrs<EV>(smem));
+  if (e == cudaSuccess) e = column_set_attrs(E, smem);
   double* din = s.alloc<double>((size_t)p * m, e);
   uint8_t* dst = s.alloc<uint8_t>((size_t)p * m, e);
   int* dkb = s.alloc<int>(m, e);
@@ -789,14 +823,10 @@ int stateless_column_op(int device, int kind, int mode, int p, int m, const doub
   if (e == cudaSuccess) e = cudaMemcpy(din, in, sizeof(double) * (size_t)p * m, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(dst, state, (size_t)p * m, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(dkb, kbar, sizeof(int) * m, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && kind == 0) {
-    DISPATCH_E(E, k_prox_standalone<EV><<<m, kNodeThreads, smem>>>(mode, p, n2, din, dst, dkb, w, M,
-                                                                   dout));
-    e = cudaGetLastError();
-  } else if (e == cudaSuccess) {
-    DISPATCH_E(E, k_g_standalone<EV><<<m, kNodeThreads, smem>>>(mode, p, n2, din, dst, dkb, M, dout));
-    e = cudaGetLastError();
-  }
+  if (e == cudaSuccess && kind == 0)
+    e = launch_prox_standalone(E, m, smem, 0, mode, p, n2, din, dst, dkb, w, M, dout);
+  else if (e == cudaSuccess)
+    e = launch_g_standalone(E, m, smem, 0, mode, p, n2, din, dst, dkb, M, dout);
   if (e == cudaSuccess) e = cudaMemcpy(out, dout, sizeof(double) * outn, cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) {
     g_stateless_err = std::string("CUDA error: ") + cudaGetErrorString(e);

@@ -40,7 +40,7 @@ struct PassResult {
   long long node_iterations = 0;  // sum over columns of iterations
 };
 
-enum KernelClass { KC_GEMM_NN = 0, KC_GEMM_TN, KC_PROX, KC_EVAL, KC_REOPT, KC_OTHER, KC_COUNT };
+enum KernelClass { KC_GEMM_NN = 0, KC_GEMM_TN, KC_PROX, KC_EVAL, KC_REOPT, KC_PASS, KC_COUNT };
 
 class Engine {
  public:
@@ -73,6 +73,7 @@ class Engine {
   double M = 1.0, lambda2 = 1.0, L = 0.0;
   long long launches = 0;
   long long h2d_bytes = 0, d2h_bytes = 0;
+  long long reopt_iterations = 0;  // support-iterations run by the re-opt kernels
   bool timing = false;
   double kc_ms[KC_COUNT] = {0};
   double kc_flops[KC_COUNT] = {0};
@@ -85,6 +86,11 @@ class Engine {
   int fail(int code, const std::string& msg);
   int cuda_fail(cudaError_t e, const char* what);
   int step(int ma, double eta, double rho, const RelaxParams& cfg);
+  int run_pass(int m, const RelaxParams& cfg, double thr, double eta, double rho, double* dTrace,
+               int& iter, int& n_evals, long long& node_its);
+  int pass_grid_ = 0;       // CTAs of the persistent pass kernel (0: disabled)
+  size_t pass_smem_ = 0;
+  long long* dPassOut_ = nullptr;
   int evaluate(int ma, double eta, double rho, const RelaxParams& cfg, int iter, double thr,
                double* trace, int eval_idx);
   struct GemmPlan {

@@ -9,11 +9,13 @@
 // compacted out, which leaves every active column's arithmetic unchanged --
 // each output column is a function of its own input column only).
 //
-// Tiling: a CTA of 4 warps owns a BM x BN output tile (BM = 8*FM, BN = 8*FN)
-// and the 4 warps split the K dimension (k-steps interleaved inside each BK=64
+// Tiling: a CTA of NW warps owns a BM x BN output tile (BM = 8*FM, BN = 8*FN)
+// and the warps split the K dimension (k-steps interleaved inside each BK=64
 // stage), so small batches still put every warp on the DMMA pipe.  Stages are
 // filled by cp.async (zero-fill at the edges) NS deep; partial accumulators
-// are combined in a fixed order (deterministic), then the fused epilogue runs.
+// are combined in a fixed warp order (deterministic), then the fused epilogue
+// runs.  gemm_tile() is shared by the standalone kernels (4 warps) and the
+// persistent pass kernel (8 warps).
 #pragma once
 #include "device_math.cuh"
 
@@ -36,7 +38,7 @@ struct GemmArgs {
   // epilogue (NN)
   const double* y;
   int loss;
-  double* part_loss;     // [blockIdx.x * part_ld + col]
+  double* part_loss;     // [row_block * part_ld + col]
   double* part_conj;
   int part_ld;
 };
@@ -45,7 +47,7 @@ constexpr int kGemmThreads = 128;
 constexpr int kBK = 64;
 constexpr int kBKP = kBK + 4;  // padded k-stride (2 wavefronts per fragment load)
 
-template <bool TN, int FM, int FN>
+template <bool TN, int FM, int FN, int NW = 4>
 struct GemmShape {
   static constexpr int BM = 8 * FM, BN = 8 * FN;
   static constexpr int PADA = (BM % 16 == 0) ? 8 : 0;  // NN: (BM+PADA) = 8 mod 16
@@ -53,32 +55,28 @@ struct GemmShape {
   static constexpr int B_ELEMS = BN * kBKP;
   static constexpr int STAGE = A_ELEMS + B_ELEMS;
   static constexpr int NS = (FM * FN >= 16) ? 3 : 4;
-  static constexpr int RED = 4 * FM * FN * 64;      // cross-warp reduction buffer
+  static constexpr int RED = NW * FM * FN * 64;     // cross-warp reduction buffer
   static constexpr int EPI = 2 * BM * BN;           // l / l* staging for EVAL
   static constexpr int SMEM_ELEMS =
       (NS * STAGE > RED + EPI) ? NS * STAGE : RED + EPI;
   static constexpr size_t SMEM_BYTES = sizeof(double) * SMEM_ELEMS;
 };
 
-template <bool TN, int FM, int FN, int EPI>
-__global__ void __launch_bounds__(kGemmThreads)
-    k_gemm(GemmArgs g) {
-  using Sh = GemmShape<TN, FM, FN>;
-  constexpr int BM = Sh::BM, BN = Sh::BN, NS = Sh::NS;
-  extern __shared__ __align__(16) double smem[];
-
-  const int ncols = *g.d_ncols;
-  const int n0 = blockIdx.y * BN;
-  if (n0 >= ncols) return;
-  const int m0 = blockIdx.x * BM;
-  const int split = blockIdx.z;
+// One output tile (mt, nt) of K-split `split`.  All NW*32 threads call.
+// colmap: 32 ints of shared memory.  Ends with a barrier (smem reusable).
+template <bool TN, int FM, int FN, int EPI, int NW>
+__device__ __forceinline__ void gemm_tile(const GemmArgs& g, int ncols, int mt, int nt, int split,
+                                          double* smem, int* colmap) {
+  using Sh = GemmShape<TN, FM, FN, NW>;
+  constexpr int BM = Sh::BM, BN = Sh::BN, NS = Sh::NS, NT = NW * 32;
+  static_assert(16 % NW == 0, "k-steps per stage must split evenly over the warps");
+  const int n0 = nt * BN;
+  const int m0 = mt * BM;
   const int kbeg = split * g.ksplit;
   const int kend = min(g.K, kbeg + g.ksplit);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  // physical columns of this tile (BN <= 32)
-  __shared__ int colmap[32];
-  if (tid < BN) {
+  if (tid < BN) {  // physical columns of this tile (BN <= 32)
     const int c = n0 + tid;
     colmap[tid] = c < ncols ? (g.act ? g.act[c] : c) : -1;
   }
@@ -89,7 +87,7 @@ __global__ void __launch_bounds__(kGemmThreads)
     double* Bs = As + Sh::A_ELEMS;
     const int k0 = kbeg + kt * kBK;
 #pragma unroll 4
-    for (int e = tid; e < BM * kBK; e += kGemmThreads) {
+    for (int e = tid; e < BM * kBK; e += NT) {
       int m, k;
       if (TN) {
         m = e / kBK;
@@ -106,7 +104,7 @@ __global__ void __launch_bounds__(kGemmThreads)
       cp_async_8(dst, src, valid);
     }
 #pragma unroll 4
-    for (int e = tid; e < BN * kBK; e += kGemmThreads) {
+    for (int e = tid; e < BN * kBK; e += NT) {
       const int c = e / kBK, k = e % kBK;
       const int gk = k0 + k;
       const int col = colmap[c];
@@ -136,8 +134,8 @@ __global__ void __launch_bounds__(kGemmThreads)
     const double* As = smem + (kt % NS) * Sh::STAGE;
     const double* Bs = As + Sh::A_ELEMS;
 #pragma unroll
-    for (int s4 = 0; s4 < kBK / 16; ++s4) {
-      const int kk = (s4 * 4 + warp) * 4 + (lane & 3);
+    for (int s4 = 0; s4 < 16 / NW; ++s4) {
+      const int kk = (s4 * NW + warp) * 4 + (lane & 3);
       double a[FM], b[FN];
 #pragma unroll
       for (int i = 0; i < FM; ++i) {
@@ -168,14 +166,15 @@ __global__ void __launch_bounds__(kGemmThreads)
   double* lv = smem + Sh::RED;
   double* cv = lv + BM * BN;
   double* Cout = g.C + (size_t)split * g.split_stride;
-  for (int e = tid; e < BM * BN; e += kGemmThreads) {
+  for (int e = tid; e < BM * BN; e += NT) {
     const int c = e / BM, r = e % BM;
     const int i = r >> 3, j = c >> 3;
     const int ln = (r & 7) * 4 + ((c & 7) >> 1), h = c & 1;
     const int off = (i * FN + j) * 64 + h * 32 + ln;
-    const int stride_w = FM * FN * 64;
-    const double s = ((red[off] + red[off + stride_w]) + red[off + 2 * stride_w]) +
-                     red[off + 3 * stride_w];
+    constexpr int stride_w = FM * FN * 64;
+    double s = red[off];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) s += red[off + w * stride_w];
     const int gm = m0 + r;
     const int col = colmap[c];
     if (EPI == EPI_STORE) {
@@ -205,10 +204,21 @@ __global__ void __launch_bounds__(kGemmThreads)
         sl += lv[tid * BM + r];
         sc += cv[tid * BM + r];
       }
-      g.part_loss[(size_t)blockIdx.x * g.part_ld + colmap[tid]] = sl;
-      g.part_conj[(size_t)blockIdx.x * g.part_ld + colmap[tid]] = sc;
+      g.part_loss[(size_t)mt * g.part_ld + colmap[tid]] = sl;
+      g.part_conj[(size_t)mt * g.part_ld + colmap[tid]] = sc;
     }
   }
+  __syncthreads();
+}
+
+template <bool TN, int FM, int FN, int EPI>
+__global__ void __launch_bounds__(kGemmThreads) k_gemm(GemmArgs g) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int colmap[32];
+  const int ncols = *g.d_ncols;
+  if ((int)blockIdx.y * GemmShape<TN, FM, FN>::BN >= ncols) return;
+  gemm_tile<TN, FM, FN, EPI, kGemmThreads / 32>(g, ncols, blockIdx.x, blockIdx.y, blockIdx.z, smem,
+                                                colmap);
 }
 
 }  // namespace bnbg

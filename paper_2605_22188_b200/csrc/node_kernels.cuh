@@ -388,7 +388,7 @@ __device__ __forceinline__ ColSmem col_smem(double* sm, int p, int n2, int E) {
 // VK1 packer: dense CoordState column + reduced budget + free count, and the
 // warm start copied into B and V.  Lists are CSR over the batch.
 // ---------------------------------------------------------------------------
-__global__ void k_pack(int p, int k, int m, const int* z_off, const int* z_idx, const int* o_off,
+static __global__ void k_pack(int p, int k, int m, const int* z_off, const int* z_idx, const int* o_off,
                        const int* o_idx, uint8_t* state, int* kbar, int* pf, const double* warm,
                        double* B, double* V, double* t, double* best, double* last_gap,
                        uint8_t* frozen, int* status, int* iters, int* act, int max_it) {
@@ -420,7 +420,7 @@ __global__ void k_pack(int p, int k, int m, const int* z_off, const int* z_idx, 
 }
 
 // init for the raw-state API (bnbg_relax_batch): state/kbar/B given.
-__global__ void k_init_cols(int p, int m, const uint8_t* state, int* pf, const double* B, double* V,
+static __global__ void k_init_cols(int p, int m, const uint8_t* state, int* pf, const double* B, double* V,
                             double* t, double* best, double* last_gap, uint8_t* frozen, int* status,
                             int* iters, int* act, int max_it) {
   __shared__ double red[kNodeThreads / 32];
@@ -448,10 +448,7 @@ __global__ void k_init_cols(int p, int m, const uint8_t* state, int* pf, const d
 // VK5: proximal-gradient step + FISTA momentum for every active column.
 // ---------------------------------------------------------------------------
 template <int E>
-__global__ void __launch_bounds__(kNodeThreads) k_prox_fista(RelaxDev r) {
-  extern __shared__ __align__(16) double sm[];
-  const int c = blockIdx.x;
-  if (c >= *r.d_ma) return;
+__device__ void prox_column(const RelaxDev& r, int c, double* sm) {
   const int b = r.act[c];
   const int p = r.p;
   const ColSmem S = col_smem(sm, p, r.n2, E);
@@ -506,6 +503,14 @@ __global__ void __launch_bounds__(kNodeThreads) k_prox_fista(RelaxDev r) {
     Bb[j] = out;
   }
   if (threadIdx.x == 0 && r.accel) r.t[b] = t_next;
+  __syncthreads();
+}
+
+template <int E>
+__global__ void __launch_bounds__(kNodeThreads) k_prox_fista(RelaxDev r) {
+  extern __shared__ __align__(16) double sm[];
+  if ((int)blockIdx.x >= *r.d_ma) return;
+  prox_column<E>(r, blockIdx.x, sm);
 }
 
 // ---------------------------------------------------------------------------
@@ -642,10 +647,7 @@ struct EvalArgs {
 };
 
 template <int E>
-__global__ void __launch_bounds__(kNodeThreads) k_eval(RelaxDev r, EvalArgs e) {
-  extern __shared__ __align__(16) double sm[];
-  const int c = blockIdx.x;
-  if (c >= *r.d_ma) return;
+__device__ void eval_column(const RelaxDev& r, const EvalArgs& e, int c, double* sm) {
   const int b = r.act[c];
   const int p = r.p;
   const ColSmem S = col_smem(sm, p, r.n2, E);
@@ -702,16 +704,25 @@ __global__ void __launch_bounds__(kNodeThreads) k_eval(RelaxDev r, EvalArgs e) {
     double* Vb = r.V + (size_t)b * p;
     for (int j = threadIdx.x; j < p; j += kNodeThreads) Vb[j] = Bb[j];
   }
+  __syncthreads();
 }
 
-// order-preserving compaction of the active list (single CTA)
-__global__ void __launch_bounds__(1024) k_compact(int* act, int* d_ma, const uint8_t* frozen) {
+template <int E>
+__global__ void __launch_bounds__(kNodeThreads) k_eval(RelaxDev r, EvalArgs e) {
+  extern __shared__ __align__(16) double sm[];
+  if ((int)blockIdx.x >= *r.d_ma) return;
+  eval_column<E>(r, e, blockIdx.x, sm);
+}
+
+// order-preserving compaction of the active list by one CTA of NT threads
+template <int NT>
+__device__ void compact_active(int* act, int* d_ma, const uint8_t* frozen) {
   __shared__ int warp_tot[32];
   __shared__ int s_base;
-  const int ma = *d_ma;
+  const int ma = *(volatile int*)d_ma;
   if (threadIdx.x == 0) s_base = 0;
   __syncthreads();
-  for (int base = 0; base < ma; base += 1024) {
+  for (int base = 0; base < ma; base += NT) {
     const int i = base + threadIdx.x;
     int a = -1;
     int keep = 0;
@@ -729,14 +740,19 @@ __global__ void __launch_bounds__(1024) k_compact(int* act, int* d_ma, const uin
     const int base_out = s_base;
     __syncthreads();
     if (keep) act[base_out + off + pre] = a;
-    if (threadIdx.x == 1023) {
+    if (threadIdx.x == NT - 1) {
       int tot = 0;
-      for (int w = 0; w < 32; ++w) tot += warp_tot[w];
+      for (int w = 0; w < NT / 32; ++w) tot += warp_tot[w];
       s_base = base_out + tot;
     }
     __syncthreads();
   }
   if (threadIdx.x == 0) *d_ma = s_base;
+  __syncthreads();
+}
+
+static __global__ void __launch_bounds__(1024) k_compact(int* act, int* d_ma, const uint8_t* frozen) {
+  compact_active<1024>(act, d_ma, frozen);
 }
 
 // ---------------------------------------------------------------------------

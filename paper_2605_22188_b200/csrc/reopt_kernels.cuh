@@ -19,7 +19,7 @@ constexpr int kReoptThreads = 256;
 __global__ void __launch_bounds__(kReoptThreads)
     k_reopt(int n, const double* __restrict__ X, const double* __restrict__ y, int loss, double M,
             double lambda2, double step, const int* off, const int* sidx, double* deriv_scratch,
-            double* coef_out, double* obj_out) {
+            double* coef_out, double* obj_out, int* it_out) {
   extern __shared__ __align__(16) double sm[];
   constexpr int NW = kReoptThreads / 32;
   const int s = blockIdx.x;
@@ -35,8 +35,10 @@ __global__ void __launch_bounds__(kReoptThreads)
   for (int r = tid; r < q; r += kReoptThreads) beta[r] = 0.0;
   if (tid == 0) s_stop = 0;
   __syncthreads();
+  int its = 0;
   if (q > 0) {
     for (int it = 0; it < 5000; ++it) {
+      ++its;
       // scores and derivative for this thread's rows (primal_heuristics.hpp:194-209)
       for (int i = tid; i < n; i += kReoptThreads) {
         double sc = 0.0;
@@ -95,6 +97,7 @@ __global__ void __launch_bounds__(kReoptThreads)
     double obj = lambda2 * sq;
     for (int w = 0; w < NW; ++w) obj += wred[w];
     obj_out[s] = obj;
+    if (it_out) it_out[s] = its;
   }
   for (int r = tid; r < q; r += kReoptThreads) coef_out[off[s] + r] = beta[r];
 }
@@ -115,7 +118,7 @@ template <int QMAX>
 __global__ void __launch_bounds__(kReoptFastThreads)
     k_reopt_direct(int n, const double* __restrict__ X, const double* __restrict__ y, int loss,
                    double M, double lambda2, double step, const int* off, const int* sidx,
-                   double* deriv_scratch, double* coef_out, double* obj_out) {
+                   double* deriv_scratch, double* coef_out, double* obj_out, int* it_out) {
   constexpr int NW = kReoptFastThreads / 32;
   __shared__ double red[2][NW][QMAX];
   __shared__ const double* cols[QMAX];
@@ -130,8 +133,10 @@ __global__ void __launch_bounds__(kReoptFastThreads)
 #pragma unroll
   for (int r = 0; r < QMAX; ++r) beta[r] = 0.0;
   int buf = 0;
+  int its = 0;
   if (q > 0) {
     for (int it = 0; it < 5000; ++it) {
+      ++its;
       double part[QMAX];
 #pragma unroll
       for (int r = 0; r < QMAX; ++r) part[r] = 0.0;
@@ -195,6 +200,7 @@ __global__ void __launch_bounds__(kReoptFastThreads)
     double obj = lambda2 * sq;
     for (int w = 0; w < NW; ++w) obj += wred[w];
     obj_out[s] = obj;
+    if (it_out) it_out[s] = its;
 #pragma unroll
     for (int r = 0; r < QMAX; ++r)
       if (r < q) coef_out[off[s] + r] = beta[r];
@@ -208,7 +214,7 @@ __global__ void __launch_bounds__(kReoptFastThreads)
 __global__ void __launch_bounds__(kReoptFastThreads)
     k_reopt_gram(int n, const double* __restrict__ X, const double* __restrict__ y, double M,
                  double lambda2, double step, const int* off, const int* sidx, double* coef_out,
-                 double* obj_out) {
+                 double* obj_out, int* it_out) {
   constexpr int NW = kReoptFastThreads / 32;
   __shared__ double gram[32][33];
   __shared__ double xty[32];
@@ -255,10 +261,12 @@ __global__ void __launch_bounds__(kReoptFastThreads)
     }
   }
   __syncthreads();
+  int its = 0;
   if (warp == 0 && q > 0) {
     double b = 0.0;
     const bool own = lane < q;
     for (int it = 0; it < 5000; ++it) {
+      ++its;
       double g = 0.0;
       for (int c = 0; c < q; ++c) {
         const double bc = __shfl_sync(0xffffffffu, b, c);
@@ -298,6 +306,7 @@ __global__ void __launch_bounds__(kReoptFastThreads)
     double obj = lambda2 * sq;
     for (int w = 0; w < NW; ++w) obj += wred[w];
     obj_out[s] = obj;
+    if (it_out) it_out[s] = its;
   }
   if (tid < q) coef_out[off[s] + tid] = bsh[tid];
 }
