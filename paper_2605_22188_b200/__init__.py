@@ -367,6 +367,14 @@ class Engine:
             out[name] = (ms.value, fl.value, ln.value)
         return out
 
+    PASS_PHASES = ("xv", "xtr", "prox", "eval_xb", "eval_xtz", "eval_cols", "compact")
+
+    def pass_profile(self):
+        """{phase: ms} of the persistent pass kernel (needs BNBG_PASS_PROF=1 at create)."""
+        buf = np.zeros(len(self.PASS_PHASES))
+        c = _L.lib().bnbg_pass_profile(self._h, buf, len(buf))
+        return {nm: buf[i] / 1e6 for i, nm in enumerate(self.PASS_PHASES[:max(c, 0)])}
+
     def transfer_bytes(self):
         a, b = C.c_longlong(), C.c_longlong()
         _L.lib().bnbg_transfer_bytes(self._h, C.byref(a), C.byref(b))

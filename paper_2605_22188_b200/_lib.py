@@ -59,6 +59,7 @@ EXPORTS = [
     "bnbg_g_value", "bnbg_g_conjugate", "bnbg_gemm", "bnbg_solve", "bnbg_collect_rashomon",
     "bnbg_pool_size", "bnbg_pool_record", "bnbg_pool_free", "bnbg_kernel_launches",
     "bnbg_gemm_stats", "bnbg_set_timing", "bnbg_kernel_stats", "bnbg_transfer_bytes",
+    "bnbg_pass_profile",
 ]
 
 
@@ -111,5 +112,6 @@ def lib():
     L.bnbg_set_timing.restype = None
     L.bnbg_kernel_stats.argtypes = [vp, i, C.POINTER(d), C.POINTER(d), C.POINTER(ll)]
     L.bnbg_transfer_bytes.argtypes = [vp, C.POINTER(ll), C.POINTER(ll)]
+    L.bnbg_pass_profile.argtypes = [vp, dp, i]
     _lib = L
     return L

@@ -708,6 +708,10 @@ int bnbg_kernel_stats(const bnbg_handle* h, int kc, double* ms, double* flops,
   return BNBG_OK;
 }
 
+int bnbg_pass_profile(const bnbg_handle* h, double* ns_out, int count) {
+  return const_cast<bnbg_handle*>(h)->eng.pass_profile(ns_out, count);
+}
+
 int bnbg_transfer_bytes(const bnbg_handle* h, long long* h2d, long long* d2h) {
   if (h2d) *h2d = h->eng.h2d_bytes;
   if (d2h) *d2h = h->eng.d2h_bytes;

@@ -59,6 +59,7 @@ Engine::~Engine() {
   cudaFree(dJb_);
   cudaFree(dAux_);
   cudaFree(dPassOut_);
+  cudaFree(dPassProf_);
   if (hPin_) cudaFreeHost(hPin_);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
@@ -115,6 +116,11 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
       if (nb >= 1) pass_grid_ = sms_;
     }
     CK(cudaMalloc(&dPassOut_, 4 * sizeof(long long)));
+    const char* penv = getenv("BNBG_PASS_PROF");
+    if (penv && penv[0] == '1') {
+      CK(cudaMalloc(&dPassProf_, 16 * sizeof(unsigned long long)));
+      CK(cudaMemsetAsync(dPassProf_, 0, 16 * sizeof(unsigned long long), stream_));
+    }
   }
   nrb_max_ = (n + 15) / 16;
   CK(cudaStreamSynchronize(stream_));
@@ -527,11 +533,13 @@ int Engine::run_pass(int m, const RelaxParams& cfg, double thr, double eta, doub
   a.prune_thr = thr;
   a.trace = dTrace;
   a.out = dPassOut_;
+  a.prof = dPassProf_;
   tic(KC_PASS);
   cudaError_t e = cudaSuccess;
   e = pass_launch(colE_, pass_grid_, pass_smem_, stream_, &a);
   ++launches;
   CK(e);
+  toc(KC_PASS, 0.0);  // end event right behind the kernel, before the readback sync
   long long h_out[4] = {0, 0, 0, 0};
   if (int rc = d2h(h_out, dPassOut_, 3 * sizeof(long long))) return rc;
   if (int rc = d2h(hPin_ + 1, dErr_, sizeof(int))) return rc;
@@ -540,7 +548,7 @@ int Engine::run_pass(int m, const RelaxParams& cfg, double thr, double eta, doub
   n_evals = (int)h_out[1];
   node_its = h_out[2];
   // algorithmic FP64 work: 4np per node-iteration (X V and X'R) -- evaluations excluded
-  toc(KC_PASS, 4.0 * n * p * (double)node_its);
+  kc_flops[KC_PASS] += 4.0 * n * p * (double)node_its;
   resolve_timing();
   if (hPin_[1] != 0x7fffffff)
     return fail(2, "relaxation: non-finite iterate in column " + std::to_string(hPin_[1]));
@@ -737,6 +745,7 @@ int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coe
                                                     d_idx, d_scr, d_coef, d_obj, d_its);
     CKL("k_reopt");
   }
+  toc(KC_REOPT, 0.0);
   std::vector<int> its(nsup);
   if (tot) if (int rc_ = d2h(coef, d_coef, sizeof(double) * tot)) return rc_;
   if (int rc_ = d2h(obj, d_obj, sizeof(double) * nsup)) return rc_;
@@ -748,9 +757,18 @@ int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coe
     flops += 4.0 * (offsets[s + 1] - offsets[s]) * (double)n * its[s];
     reopt_iterations += its[s];
   }
-  toc(KC_REOPT, flops);
+  kc_flops[KC_REOPT] += flops;
   resolve_timing();
   return 0;
+}
+
+int Engine::pass_profile(double* ns, int count) {
+  if (!dPassProf_) return 0;
+  unsigned long long h[16];
+  CK(cudaMemcpy(h, dPassProf_, sizeof(h), cudaMemcpyDeviceToHost));
+  const int c = std::min(count, 7);
+  for (int i = 0; i < c; ++i) ns[i] = (double)h[i];
+  return c;
 }
 
 int Engine::gemm_probe(int trans, int m, const double* Bh, double* Ch) {

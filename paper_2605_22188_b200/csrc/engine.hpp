@@ -91,6 +91,10 @@ class Engine {
   int pass_grid_ = 0;       // CTAs of the persistent pass kernel (0: disabled)
   size_t pass_smem_ = 0;
   long long* dPassOut_ = nullptr;
+ public:
+  unsigned long long* dPassProf_ = nullptr;  // phase wall times (BNBG_PASS_PROF=1)
+  int pass_profile(double* ns, int count);
+ private:
   int evaluate(int ma, double eta, double rho, const RelaxParams& cfg, int iter, double thr,
                double* trace, int eval_idx);
   struct GemmPlan {

@@ -20,6 +20,7 @@ struct PassArgs {
   double gap_tol, prune_thr;
   double* trace;
   long long* out;  // [0] iterations, [1] evaluations, [2] node-iterations
+  unsigned long long* prof;  // optional phase wall times (ns, CTA 0's view); nullptr: off
 };
 
 // ---- gemm_kernels.cu -------------------------------------------------------

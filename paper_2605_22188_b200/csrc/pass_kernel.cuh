@@ -91,6 +91,15 @@ __host__ inline size_t pass_smem_bytes(int p, int n2, int E) {
   return b;
 }
 
+__device__ __forceinline__ unsigned long long pass_clock() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// phase wall-time accumulation (tools/profile_solve.py; off in the product)
+enum { PH_NN = 0, PH_TN, PH_PROX, PH_EVNN, PH_EVTN, PH_EVCOL, PH_COMPACT, PH_COUNT };
+
 template <int E>
 __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a) {
   extern __shared__ __align__(16) double smem[];
@@ -100,12 +109,23 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a) {
   int iter = 0, last_eval = 0, n_evals = 0;
   long long node_its = 0;
   int ma = *(volatile int*)r.d_ma;
+  const bool prof = a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long t_last = prof ? pass_clock() : 0ull;
+  auto mark = [&](int ph) {
+    if (prof) {
+      const unsigned long long t = pass_clock();
+      a.prof[ph] += t - t_last;
+      t_last = t;
+    }
+  };
 
   auto evaluate = [&](int it) {  // relaxation.hpp:194-221
     pass_phase_nn<EPI_EVAL>(a, r.B, ma, smem, colmap);
     grid.sync();
+    mark(PH_EVNN);
     r.nsplit = pass_phase_tn(a, ma, smem, colmap);
     grid.sync();
+    mark(PH_EVTN);
     EvalArgs e;
     e.part_loss = a.nn.part_loss;
     e.part_conj = a.nn.part_conj;
@@ -118,8 +138,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a) {
     e.eval_idx = n_evals;
     for (int c = blockIdx.x; c < ma; c += gridDim.x) eval_column<E>(r, e, c, smem);
     grid.sync();
+    mark(PH_EVCOL);
     if (blockIdx.x == 0) compact_active<kPassThreads>(r.act, r.d_ma, r.frozen);
     grid.sync();
+    mark(PH_COMPACT);
     ma = *(volatile int*)r.d_ma;
     // non-finite iterate (numeric_error, relaxation.hpp:76-81): stop early;
     // the host reports the column from d_err
@@ -131,10 +153,13 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a) {
     ++iter;
     pass_phase_nn<EPI_DERIV>(a, r.V, ma, smem, colmap);
     grid.sync();
+    mark(PH_NN);
     r.nsplit = pass_phase_tn(a, ma, smem, colmap);
     grid.sync();
+    mark(PH_TN);
     for (int c = blockIdx.x; c < ma; c += gridDim.x) prox_column<E>(r, c, smem);
     grid.sync();
+    mark(PH_PROX);
     node_its += ma;
     if (iter % a.check == 0) {
       evaluate(iter);
