@@ -708,9 +708,34 @@ int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coe
   int qmax = 0;
   for (int s = 0; s < nsup; ++s) qmax = std::max(qmax, offsets[s + 1] - offsets[s]);
   const bool gram = loss == kSquared && qmax <= 32;
-  const bool direct = !gram && qmax <= 16;
+  // cluster gather form: X_S slice in registers, CS CTAs per support
+  int cs = 0, rpt = 0;
+  if (!gram && qmax <= 16) {
+    const int qm = qmax <= 8 ? 8 : 16;
+    const int rpt_max = 64 / qm;
+    for (int c = 1; c <= kReoptMaxCluster; c <<= 1) {
+      const int rows = (n + c - 1) / c;
+      const int need = (rows + kReoptClusterThreads - 1) / kReoptClusterThreads;
+      if (need <= rpt_max) {
+        cs = c;
+        break;
+      }
+    }
+    if (cs) {
+      const char* env = getenv("BNBG_REOPT_CS");
+      if (env && atoi(env) > 0) {
+        cs = std::max(cs, std::min(kReoptMaxCluster, atoi(env)));
+      } else {
+        while (cs < kReoptMaxCluster && nsup * cs * 2 <= sms_) cs <<= 1;
+      }
+      const int rows = (n + cs - 1) / cs;
+      const int need = (rows + kReoptClusterThreads - 1) / kReoptClusterThreads;
+      rpt = need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : 8;
+    }
+  }
+  const bool direct = !gram && !cs && qmax <= 16;
   // the deriv scratch is only used by the generic kernel
-  const size_t scr = (gram || direct) ? 0 : (size_t)nsup * n;
+  const size_t scr = (gram || direct || cs) ? 0 : (size_t)nsup * n;
   const size_t bytes = sizeof(double) * (scr + tot + nsup + 2) +
                        sizeof(int) * ((size_t)2 * nsup + 1 + tot + 2);
   if (int rc = ensure_aux(bytes)) return rc;
@@ -728,6 +753,10 @@ int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coe
     k_reopt_gram<<<nsup, kReoptFastThreads, 0, stream_>>>(n, dX_, dy_, M, lambda2, step, d_off,
                                                           d_idx, d_coef, d_obj, d_its);
     CKL("k_reopt_gram");
+  } else if (cs) {
+    ++launches;
+    CK(launch_reopt_cluster(qmax <= 8 ? 8 : 16, rpt, cs, nsup, stream_, n, dX_, dy_, loss, M,
+                            lambda2, step, d_off, d_idx, d_coef, d_obj, d_its));
   } else if (qmax <= 8) {
     k_reopt_direct<8><<<nsup, kReoptFastThreads, 0, stream_>>>(
         n, dX_, dy_, loss, M, lambda2, step, d_off, d_idx, d_scr, d_coef, d_obj, d_its);

@@ -45,6 +45,13 @@ cudaError_t launch_g_standalone(int E, int m, size_t smem, cudaStream_t st, int 
                                 const double* in, const uint8_t* state, const int* kbar, double M,
                                 double* out);
 
+// ---- reopt_kernels.cu ------------------------------------------------------
+// k_reopt_cluster<qmax in {8,16}, rpt>: cs CTAs (one cluster) per support
+cudaError_t launch_reopt_cluster(int qmax, int rpt, int cs, int nsup, cudaStream_t st, int n,
+                                 const double* X, const double* y, int loss, double M,
+                                 double lambda2, double step, const int* off, const int* idx,
+                                 double* coef, double* obj, int* its);
+
 // ---- pass_kernels.cu -------------------------------------------------------
 size_t pass_smem(int p, int n2, int E);
 cudaError_t pass_setup(int E, size_t smem, int* blocks_per_sm);

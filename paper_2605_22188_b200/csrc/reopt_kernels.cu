@@ -1,0 +1,41 @@
+// reopt_kernels.cu -- instantiations and cluster launcher of k_reopt_cluster.
+#include "launchers.hpp"
+#include "reopt_kernels.cuh"
+
+namespace bnbg {
+
+template <int Q, int R>
+static cudaError_t launch_q_r(int cs, int nsup, cudaStream_t st, int n, const double* X,
+                              const double* y, int loss, double M, double lambda2, double step,
+                              const int* off, const int* idx, double* coef, double* obj,
+                              int* its) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nsup * cs);
+  cfg.blockDim = dim3(kReoptClusterThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_reopt_cluster<Q, R>, n, X, y, loss, M, lambda2, step, off, idx,
+                            coef, obj, its);
+}
+
+cudaError_t launch_reopt_cluster(int qmax, int rpt, int cs, int nsup, cudaStream_t st, int n,
+                                 const double* X, const double* y, int loss, double M,
+                                 double lambda2, double step, const int* off, const int* idx,
+                                 double* coef, double* obj, int* its) {
+#define RQ(Q, R)                                                                              \
+  if (qmax == Q && rpt == R)                                                                  \
+    return launch_q_r<Q, R>(cs, nsup, st, n, X, y, loss, M, lambda2, step, off, idx, coef, obj, \
+                            its);
+  RQ(8, 1) RQ(8, 2) RQ(8, 4) RQ(8, 8) RQ(16, 1) RQ(16, 2) RQ(16, 4)
+#undef RQ
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace bnbg

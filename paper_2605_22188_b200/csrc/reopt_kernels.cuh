@@ -5,6 +5,8 @@
 //   k_gemv_n / k_gemv_t / k_power_stats / k_scale   smoothness_constant
 //                                  power iteration (losses.hpp:86-112)
 #pragma once
+#include <cooperative_groups.h>
+
 #include "device_math.cuh"
 
 namespace bnbg {
@@ -16,7 +18,7 @@ namespace bnbg {
 // --------------------------------------------------------------------------
 constexpr int kReoptThreads = 256;
 
-__global__ void __launch_bounds__(kReoptThreads)
+static __global__ void __launch_bounds__(kReoptThreads)
     k_reopt(int n, const double* __restrict__ X, const double* __restrict__ y, int loss, double M,
             double lambda2, double step, const int* off, const int* sidx, double* deriv_scratch,
             double* coef_out, double* obj_out, int* it_out) {
@@ -207,11 +209,167 @@ __global__ void __launch_bounds__(kReoptFastThreads)
   }
 }
 
+// --------------------------------------------------------------------------
+// k_reopt_cluster: the gather form split over a thread-block cluster of CS
+// CTAs (CS = 1..8, chosen at launch).  CTA `rank` owns rows
+// [rank*chunk, (rank+1)*chunk) and keeps its slice of X_S and y in registers
+// for all 5000 iterations (RPT rows per thread), so an iteration touches no
+// memory: per-row scores / l' / gradient partials, a warp-shuffle and
+// cross-warp reduction, then the CTA partials are exchanged through
+// distributed shared memory and one cluster barrier.  Every CTA sums the
+// partials in rank order and redoes the q-vector update, so all CTAs hold the
+// same beta and take the same stopping decision.  Partial buffers alternate
+// per iteration, which makes one cluster barrier per iteration sufficient.
+// --------------------------------------------------------------------------
+constexpr int kReoptClusterThreads = 128;
+constexpr int kReoptMaxCluster = 8;
+
+// Warp reduce-scatter of QMAX partial sums (QMAX in {8, 16}): log2(QMAX)
+// halving exchanges, then a butterfly over the remaining lane bits -- 9
+// shuffles for QMAX = 8 instead of 40.  On return v[0] of lane L holds the
+// warp total of value reduce_scatter_index<QMAX>(L).
+template <int QMAX>
+__device__ __forceinline__ int reduce_scatter_index(int lane) {
+  return QMAX == 8 ? (lane >> 2) & 7 : (lane >> 1) & 15;
+}
+template <int QMAX>
+__device__ __forceinline__ void warp_reduce_scatter(double (&v)[QMAX], int lane) {
+  constexpr int LOGQ = QMAX == 8 ? 3 : 4;
+#pragma unroll
+  for (int l = 0; l < LOGQ; ++l) {
+    const int o = 16 >> l;
+    const int half = QMAX >> (l + 1);
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int r = 0; r < half; ++r) {
+      const double send = up ? v[r] : v[r + half];
+      const double keep = up ? v[r + half] : v[r];
+      v[r] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+#pragma unroll
+  for (int o = 16 >> LOGQ; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+}
+
+template <int QMAX, int RPT>
+__global__ void __launch_bounds__(kReoptClusterThreads)
+    k_reopt_cluster(int n, const double* __restrict__ X, const double* __restrict__ y, int loss,
+                    double M, double lambda2, double step, const int* off, const int* sidx,
+                    double* coef_out, double* obj_out, int* it_out) {
+  namespace cg = cooperative_groups;
+  constexpr int NT = kReoptClusterThreads, NW = NT / 32;
+  cg::cluster_group cl = cg::this_cluster();
+  const int CS = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  const int s = blockIdx.x / CS;
+  __shared__ double red[2][NW][QMAX];
+  __shared__ __align__(16) double xsum[2][kReoptMaxCluster][QMAX];
+  __shared__ double fin[kReoptMaxCluster];
+  __shared__ double wred[NW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = off[s + 1] - off[s];
+  const int* S = sidx + off[s];
+  const int chunk = (n + CS - 1) / CS;
+  const int r0 = rank * chunk, r1 = min(n, r0 + chunk);
+  double xs[RPT][QMAX], ys[RPT];
+  bool valid[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int i = r0 + j * NT + tid;
+    valid[j] = i < r1;
+    ys[j] = valid[j] ? y[i] : 0.0;
+#pragma unroll
+    for (int r = 0; r < QMAX; ++r) xs[j][r] = (valid[j] && r < q) ? X[(size_t)S[r] * n + i] : 0.0;
+  }
+  double beta[QMAX];
+#pragma unroll
+  for (int r = 0; r < QMAX; ++r) beta[r] = 0.0;
+  const int ridx = reduce_scatter_index<QMAX>(lane);
+  const bool writer = (lane & (32 / QMAX - 1)) == 0;
+  int buf = 0, its = 0;
+  if (q > 0) {
+    for (int it = 0; it < 5000; ++it) {
+      ++its;
+      double part[QMAX];
+#pragma unroll
+      for (int r = 0; r < QMAX; ++r) part[r] = 0.0;
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        double sc = 0.0;  // scores, r ascending (primal_heuristics.hpp:194-198)
+#pragma unroll
+        for (int r = 0; r < QMAX; ++r) sc += beta[r] * xs[j][r];
+        const double di = valid[j] ? d_loss_deriv(loss, sc, ys[j]) : 0.0;
+#pragma unroll
+        for (int r = 0; r < QMAX; ++r) part[r] += xs[j][r] * di;
+      }
+      warp_reduce_scatter<QMAX>(part, lane);
+      if (writer) red[buf][warp][ridx] = part[0];
+      __syncthreads();
+      if (tid < CS * QMAX) {  // one DSMEM store per (destination, value)
+        const int dst = tid / QMAX, r = tid % QMAX;
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) v += red[buf][w][r];
+        *cl.map_shared_rank(&xsum[buf][rank][r], dst) = v;
+      }
+      cl.sync();
+      double gs[QMAX];
+#pragma unroll
+      for (int r = 0; r < QMAX; ++r) gs[r] = 0.0;
+      for (int c = 0; c < CS; ++c) {
+        const double2* row = reinterpret_cast<const double2*>(xsum[buf][c]);
+#pragma unroll
+        for (int r2 = 0; r2 < QMAX / 2; ++r2) {
+          const double2 t = row[r2];
+          gs[2 * r2] += t.x;
+          gs[2 * r2 + 1] += t.y;
+        }
+      }
+      double gm2 = 0.0;
+#pragma unroll
+      for (int r = 0; r < QMAX; ++r) {
+        double g = gs[r];
+        g += 2.0 * lambda2 * beta[r];  // (:210-211)
+        double v = beta[r] - step * g;
+        v = v < -M ? -M : v;
+        v = v > M ? M : v;
+        const double dl = beta[r] - v;
+        gm2 += dl * dl;
+        beta[r] = r < q ? v : 0.0;
+      }
+      buf ^= 1;
+      if (sqrt(gm2) / step <= 1e-8) break;  // (:212-215)
+    }
+  }
+  // objective lambda2 |beta|^2 + sum l(X_S beta)  (:217-222)
+  double acc = 0.0;
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    double sc = 0.0;
+#pragma unroll
+    for (int r = 0; r < QMAX; ++r) sc += beta[r] * xs[j][r];
+    if (valid[j]) acc += d_loss_value(loss, sc, ys[j]);
+  }
+  const double cta = block_sum<NT>(acc, wred);
+  if (tid == 0) *cl.map_shared_rank(&fin[rank], 0) = cta;
+  cl.sync();
+  if (rank == 0 && tid == 0) {
+    double sq = 0.0;
+#pragma unroll
+    for (int r = 0; r < QMAX; ++r) sq += beta[r] * beta[r];
+    double obj = lambda2 * sq;
+    for (int c = 0; c < CS; ++c) obj += fin[c];
+    obj_out[s] = obj;
+    if (it_out) it_out[s] = its;
+    for (int r = 0; r < q && r < QMAX; ++r) coef_out[off[s] + r] = beta[r];
+  }
+}
+
 // k_reopt_gram (squared loss): X_S'(X_S beta - y) = Gram beta - X_S'y, the
 // same iterates in exact arithmetic.  The q x q Gram and
 // X_S'y are built once per support; warp 0 then runs the projected-gradient
 // loop with lane r owning beta_r.  q <= 32.
-__global__ void __launch_bounds__(kReoptFastThreads)
+static __global__ void __launch_bounds__(kReoptFastThreads)
     k_reopt_gram(int n, const double* __restrict__ X, const double* __restrict__ y, double M,
                  double lambda2, double step, const int* off, const int* sidx, double* coef_out,
                  double* obj_out, int* it_out) {
@@ -314,7 +472,7 @@ __global__ void __launch_bounds__(kReoptFastThreads)
 // --------------------------------------------------------------------------
 // smoothness constant (losses.hpp:86-112): power-iteration GEMVs
 // --------------------------------------------------------------------------
-__global__ void k_gemv_n(int n, int p, const double* __restrict__ X, const double* __restrict__ v,
+static __global__ void k_gemv_n(int n, int p, const double* __restrict__ X, const double* __restrict__ v,
                          double* __restrict__ xv) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -323,7 +481,7 @@ __global__ void k_gemv_n(int n, int p, const double* __restrict__ X, const doubl
   xv[i] = s;
 }
 
-__global__ void k_gemv_t(int n, int p, const double* __restrict__ X, const double* __restrict__ xv,
+static __global__ void k_gemv_t(int n, int p, const double* __restrict__ X, const double* __restrict__ xv,
                          double* __restrict__ w) {
   const int j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -337,7 +495,7 @@ __global__ void k_gemv_t(int n, int p, const double* __restrict__ X, const doubl
 }
 
 // out[0] = v.w, out[1] = |w|; single CTA of 256 threads
-__global__ void k_power_stats(int p, const double* v, const double* w, double* out) {
+static __global__ void k_power_stats(int p, const double* v, const double* w, double* out) {
   __shared__ double red[8];
   double a = 0.0, c = 0.0;
   for (int j = threadIdx.x; j < p; j += 256) {
@@ -352,7 +510,7 @@ __global__ void k_power_stats(int p, const double* v, const double* w, double* o
   }
 }
 
-__global__ void k_scale(int p, const double* w, double wn, double* v) {
+static __global__ void k_scale(int p, const double* w, double wn, double* v) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < p) v[j] = w[j] / wn;
 }
