@@ -198,8 +198,10 @@ int bnbg_kernel_stats(const bnbg_handle* h, int kernel_class, double* ms, double
 /* Wall time (ns, CTA 0's view, including the grid barrier that ends each
  * phase) of the persistent pass kernel's phases since the handle was created:
  * [0] X*V, [1] X'*R, [2] prox/FISTA, [3] eval X*B, [4] eval X'*Z, [5] eval
- * columns, [6] compaction.  Recorded only when BNBG_PASS_PROF=1 was set at
- * bnbg_create; returns the number of phases written. */
+ * columns, [6] compaction; [8..14] the same phases up to CTA 0's arrival at
+ * the phase's grid barrier (the rest is barrier wait); [16..19] prox sub-phases of
+ * CTA 0 (load+sort, PAVA, scatter, end barrier).  Recorded only when
+ * BNBG_PASS_PROF=1 was set at bnbg_create; returns the number of values written. */
 int bnbg_pass_profile(const bnbg_handle* h, double* ns_out, int count);
 /* Host<->device bytes copied by this handle so far. */
 int bnbg_transfer_bytes(const bnbg_handle* h, long long* h2d, long long* d2h);

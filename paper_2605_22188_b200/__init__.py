@@ -371,9 +371,18 @@ class Engine:
 
     def pass_profile(self):
         """{phase: ms} of the persistent pass kernel (needs BNBG_PASS_PROF=1 at create)."""
-        buf = np.zeros(len(self.PASS_PHASES))
+        buf = np.zeros(16)
         c = _L.lib().bnbg_pass_profile(self._h, buf, len(buf))
-        return {nm: buf[i] / 1e6 for i, nm in enumerate(self.PASS_PHASES[:max(c, 0)])}
+        out = {nm: buf[i] / 1e6 for i, nm in enumerate(self.PASS_PHASES) if i < c}
+        out.update({nm + "_work": buf[8 + i] / 1e6 for i, nm in enumerate(self.PASS_PHASES)
+                    if 8 + i < c})
+        return out
+
+    def pass_profile_raw(self):
+        """The raw 32-slot profile buffer in ns (see bnbg_pass_profile)."""
+        buf = np.zeros(32)
+        _L.lib().bnbg_pass_profile(self._h, buf, len(buf))
+        return buf
 
     def transfer_bytes(self):
         a, b = C.c_longlong(), C.c_longlong()

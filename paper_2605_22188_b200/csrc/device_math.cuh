@@ -85,6 +85,12 @@ __device__ __forceinline__ void cp_async_8(void* smem, const void* gmem, bool va
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
                "r"(src_size));
 }
+// 16-byte copy; src_bytes in {0, 8, 16}, the rest of the 16 bytes zero-filled
+__device__ __forceinline__ void cp_async_16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -105,6 +111,30 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 #pragma unroll
   for (int w = 0; w < NT / 32; ++w) s += red[w];
   return s;
+}
+
+// Block-wide deterministic sums of NV values at once (one barrier pair).
+// `red` must hold (blockDim.x/32) * NV doubles.  All threads receive the sums.
+template <int NT, int NV>
+__device__ __forceinline__ void block_sum_vec(double (&v)[NV], double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < NV; ++r)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[r] += __shfl_xor_sync(0xffffffffu, v[r], o);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int r = 0; r < NV; ++r) red[warp * NV + r] = v[r];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < NV; ++r) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) s += red[w * NV + r];
+    v[r] = s;
+  }
 }
 
 template <int NT>

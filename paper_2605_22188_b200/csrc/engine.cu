@@ -60,6 +60,7 @@ Engine::~Engine() {
   cudaFree(dAux_);
   cudaFree(dPassOut_);
   cudaFree(dPassProf_);
+  cudaFree(dBar_);
   if (hPin_) cudaFreeHost(hPin_);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
@@ -103,23 +104,43 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
   csmem_ = column_smem_bytes(p, n2_, colE_);
   if (csmem_ > 220 * 1024) return fail(1, "p too large for the column kernels");
   CK(column_set_attrs(colE_, csmem_));
-  // persistent pass kernel: one CTA per SM when it fits (BNBG_PERSISTENT=0 disables)
+  // persistent pass kernel: one CTA per SM when it fits (BNBG_PERSISTENT=0
+  // disables it; BNBG_RESIDENT=0 forces the streaming operand mode)
   {
     const char* env = getenv("BNBG_PERSISTENT");
-    int coop = 0;
+    const char* renv = getenv("BNBG_RESIDENT");
+    int coop = 0, optin = 0;
     CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
-    pass_smem_ = pass_smem(p, n2_, colE_);
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     pass_grid_ = 0;
-    if (coop && !(env && env[0] == '0') && pass_smem_ <= 220 * 1024) {
-      int nb = 0;
-      CK(pass_setup(colE_, pass_smem_, &nb));
-      if (nb >= 1) pass_grid_ = sms_;
+    res_ = ResLayout{};
+    if (coop && !(env && env[0] == '0')) {
+      size_t stat = 0;
+      CK(pass_static_smem(colE_, &stat));
+      const size_t limit = (size_t)optin - stat - 256;
+      pass_smem_ = pass_smem(p, n2_, colE_);
+      if (!(renv && renv[0] == '0')) {
+        ResLayout L;
+        const size_t rb = pass_res_plan(n, p, n2_, colE_, sms_, limit, &L);
+        if (L.on) {
+          const char* cenv = getenv("BNBG_COLCACHE");
+          if (cenv && cenv[0] == '0') L.off_cc = 0;  // diagnostics: no column cache
+          res_ = L;
+          pass_smem_ = rb;
+        }
+      }
+      if (pass_smem_ <= limit) {
+        int nb = 0;
+        CK(pass_setup(colE_, pass_smem_, &nb));
+        if (nb >= 1) pass_grid_ = sms_;
+      }
     }
+    CK(cudaMalloc(&dBar_, sizeof(unsigned)));
     CK(cudaMalloc(&dPassOut_, 4 * sizeof(long long)));
     const char* penv = getenv("BNBG_PASS_PROF");
     if (penv && penv[0] == '1') {
-      CK(cudaMalloc(&dPassProf_, 16 * sizeof(unsigned long long)));
-      CK(cudaMemsetAsync(dPassProf_, 0, 16 * sizeof(unsigned long long), stream_));
+      CK(cudaMalloc(&dPassProf_, 32 * sizeof(unsigned long long)));
+      CK(cudaMemsetAsync(dPassProf_, 0, 32 * sizeof(unsigned long long), stream_));
     }
   }
   nrb_max_ = (n + 15) / 16;
@@ -275,7 +296,7 @@ Engine::GemmPlan Engine::plan(int Mr, int K, int ncols, bool allow_split) const 
 int Engine::launch_gemm(bool tn, int epi, const GemmPlan& pl, const double* Bsrc, int ldb,
                         double* C, int ldc, const int* act, const int* d_ncols,
                         long long split_stride, int part_ld) {
-  GemmArgs g;
+  GemmArgs g{};
   g.M = tn ? p : n;
   g.K = tn ? n : p;
   g.A = dX_;
@@ -368,7 +389,7 @@ int Engine::step(int ma, double eta, double rho, const RelaxParams& cfg) {
     return rc;
   toc(KC_GEMM_TN, 2.0 * n * p * ma);
   cur_nsplit_ = p2.nsplit;
-  RelaxDev r;
+  RelaxDev r{};
   r.p = p;
   r.n2 = n2_;
   r.mcap = mcap_;
@@ -414,7 +435,7 @@ int Engine::evaluate(int ma, double eta, double rho, const RelaxParams& cfg, int
                            (long long)p * mcap_, mcap_))
     return rc;
   toc(KC_GEMM_TN, 2.0 * n * p * ma);
-  RelaxDev r;
+  RelaxDev r{};
   r.p = p;
   r.n2 = n2_;
   r.mcap = mcap_;
@@ -471,7 +492,7 @@ int Engine::evaluate(int ma, double eta, double rho, const RelaxParams& cfg, int
 int Engine::run_pass(int m, const RelaxParams& cfg, double thr, double eta, double rho,
                      double* dTrace, int& iter, int& n_evals, long long& node_its) {
   (void)m;
-  PassArgs a;
+  PassArgs a{};
   RelaxDev& r = a.r;
   r.p = p;
   r.n2 = n2_;
@@ -534,6 +555,12 @@ int Engine::run_pass(int m, const RelaxParams& cfg, double thr, double eta, doub
   a.trace = dTrace;
   a.out = dPassOut_;
   a.prof = dPassProf_;
+  r.probe = dPassProf_ ? dPassProf_ + 16 : nullptr;
+  a.nn.probe = dPassProf_ ? dPassProf_ + 20 : nullptr;
+  a.tn.probe = dPassProf_ ? dPassProf_ + 24 : nullptr;
+  a.bar = dBar_;
+  a.res = res_;
+  CK(cudaMemsetAsync(dBar_, 0, sizeof(unsigned), stream_));
   tic(KC_PASS);
   cudaError_t e = cudaSuccess;
   e = pass_launch(colE_, pass_grid_, pass_smem_, stream_, &a);
@@ -572,7 +599,7 @@ int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_
   int iter = 0, last_eval = 0, ma = m, n_evals = 0;
   long long node_its = 0;
   int rc = 0;
-  if (pass_grid_ > 0 && m <= 2 * sms_) {
+  if (pass_grid_ > 0 && (res_.on || m <= 2 * sms_)) {
     // narrow batch: the whole relaxation as one persistent cooperative kernel
     if ((rc = run_pass(m, cfg, thr, eta, rho, dTrace, iter, n_evals, node_its))) goto done;
   } else {
@@ -793,9 +820,11 @@ int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coe
 
 int Engine::pass_profile(double* ns, int count) {
   if (!dPassProf_) return 0;
-  unsigned long long h[16];
+  unsigned long long h[32];
   CK(cudaMemcpy(h, dPassProf_, sizeof(h), cudaMemcpyDeviceToHost));
-  const int c = std::min(count, 7);
+  // [0..6] phase totals, [8..14] CTA 0's time to the phase barrier,
+  // [16..19] prox sub-phases of CTA 0 (load+sort, PAVA, scatter, barrier)
+  const int c = std::min(count, 32);
   for (int i = 0; i < c; ++i) ns[i] = (double)h[i];
   return c;
 }

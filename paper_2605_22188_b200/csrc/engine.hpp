@@ -13,6 +13,8 @@
 #include <string>
 #include <vector>
 
+#include "launchers.hpp"
+
 namespace bnbg {
 
 struct RelaxParams {
@@ -91,6 +93,8 @@ class Engine {
   int pass_grid_ = 0;       // CTAs of the persistent pass kernel (0: disabled)
   size_t pass_smem_ = 0;
   long long* dPassOut_ = nullptr;
+  unsigned* dBar_ = nullptr;  // grid barrier counter of the pass kernel
+  ResLayout res_{};           // X residency plan (res_.on = 0: streaming)
  public:
   unsigned long long* dPassProf_ = nullptr;  // phase wall times (BNBG_PASS_PROF=1)
   int pass_profile(double* ns, int count);

@@ -41,6 +41,7 @@ struct GemmArgs {
   double* part_loss;     // [row_block * part_ld + col]
   double* part_conj;
   int part_ld;
+  unsigned long long* probe;  // optional sub-phase timers (CTA 0), nullptr: off
 };
 
 constexpr int kGemmThreads = 128;

@@ -10,6 +10,24 @@
 
 namespace bnbg {
 
+// Shared-memory residency plan of X for the persistent pass kernel: CTA b
+// keeps NN row tile b (rows [16b, 16b+16) x all p, k-major, stride lda_nn)
+// and TN tile b (X columns [16 (b % tn_mt), +16) x rows of split b / tn_mt,
+// row-major, stride ldk_tn) for the whole pass; only V / R move per iteration.
+struct ResLayout {
+  int on;        // 0: stream X tiles from L2/HBM (gemm_tile)
+  int nn_tiles;  // ceil(n / 16)
+  int kpad_nn;   // p rounded up to 4
+  int lda_nn;    // 20 (conflict-free DMMA fragment loads)
+  int tn_mt;     // ceil(p / 16)
+  int tn_split;  // K splits of the n rows
+  int tn_klen;   // rows per split (multiple of 4)
+  int ldk_tn;    // >= tn_klen, = 4 mod 16
+  int ldb;       // k-stride of the staged B operand, >= max(kpad_nn, tn_klen), = 4 mod 16
+  long long off_tn, off_work;  // double offsets of the TN tile and the work region
+  long long off_cc;            // column cache (B, V, states of the CTA's column); 0: none
+};
+
 // arguments of the persistent pass kernel (pass_kernel.cuh)
 struct PassArgs {
   RelaxDev r;
@@ -21,6 +39,8 @@ struct PassArgs {
   double* trace;
   long long* out;  // [0] iterations, [1] evaluations, [2] node-iterations
   unsigned long long* prof;  // optional phase wall times (ns, CTA 0's view); nullptr: off
+  unsigned* bar;             // grid barrier counter (zeroed before the launch)
+  ResLayout res;
 };
 
 // ---- gemm_kernels.cu -------------------------------------------------------
@@ -54,7 +74,11 @@ cudaError_t launch_reopt_cluster(int qmax, int rpt, int cs, int nsup, cudaStream
 
 // ---- pass_kernels.cu -------------------------------------------------------
 size_t pass_smem(int p, int n2, int E);
+// residency plan for `grid` CTAs (res.on = 0 when X does not fit); returns the
+// dynamic shared memory the resident kernel needs
+size_t pass_res_plan(int n, int p, int n2, int E, int grid, size_t smem_limit, ResLayout* res);
 cudaError_t pass_setup(int E, size_t smem, int* blocks_per_sm);
+cudaError_t pass_static_smem(int E, size_t* bytes);
 cudaError_t pass_launch(int E, int grid, size_t smem, cudaStream_t st, PassArgs* a);
 
 }  // namespace bnbg

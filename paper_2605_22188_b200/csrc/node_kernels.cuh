@@ -52,18 +52,36 @@ struct RelaxDev {
   int* d_err;
   double eta, rho, M, lambda2;
   int accel;
+  unsigned long long* probe;  // optional sub-phase timers of CTA 0's column work (nullptr: off)
+};
+
+// CTA 0's sub-phase timer (tools/pass_phases.py); compiled in, off unless r.probe is set
+struct ColProbe {
+  unsigned long long* p;
+  unsigned long long t;
+  __device__ __forceinline__ explicit ColProbe(unsigned long long* q)
+      : p(q && blockIdx.x == 0 && threadIdx.x == 0 ? q : nullptr), t(0) {
+    if (p) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  }
+  __device__ __forceinline__ void mark(int i) {
+    if (!p) return;
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    p[i] += now - t;
+    t = now;
+  }
 };
 
 // G = sum of the split-K slabs, added in slab order (loads issued together)
-__device__ __forceinline__ double gsum(const RelaxDev& r, int b, int j) {
+__device__ __forceinline__ double gsum(const RelaxDev& r, int ns, int b, int j) {
   double part[kMaxSplit];
 #pragma unroll
   for (int s = 0; s < kMaxSplit; ++s)
-    part[s] = s < r.nsplit ? r.G[(size_t)s * r.split_stride + (size_t)b * r.p + j] : 0.0;
+    part[s] = s < ns ? r.G[(size_t)s * r.split_stride + (size_t)b * r.p + j] : 0.0;
   double g = part[0];
 #pragma unroll
   for (int s = 1; s < kMaxSplit; ++s)
-    if (s < r.nsplit) g += part[s];
+    if (s < ns) g += part[s];
   return g;
 }
 
@@ -77,11 +95,12 @@ __device__ __forceinline__ bool kv_before(double ka, int ia, double kb, int ib) 
 // number of sorted slots of the key/idx arrays
 __host__ __device__ inline int sort_slots(int n2, int E) { return E ? kNodeThreads * E : n2; }
 
-// dynamic shared memory: key[NS] idx[NS] u[p] scan[NS] (+ exchange buffers 2x(NS doubles + NS ints))
+// dynamic shared memory: key[NS] idx[NS] u[p] scan[NS] (+ exchange buffers
+// 2x(NS doubles + NS ints)) bo[p] (staged previous iterate) st[p] (staged states)
 __host__ __device__ inline size_t column_smem_bytes(int p, int n2, int E) {
   const size_t ns = (size_t)sort_slots(n2, E);
   size_t b = ns * 8 + ns * 4 + (size_t)p * 8 + ns * 8;
-  if (E) b += 2 * ns * 12;
+  if (E) b += 2 * ns * 12 + (size_t)p * 8 + (size_t)p + 16;  // staging only for register sorts
   return b + 64;
 }
 
@@ -302,60 +321,64 @@ __device__ void block_pava(const double* key, int pf, int kbar, double w, double
     const double mean_w = w * (double)(kbar - lo) / len;
     return d_prox_huber(sum / len, mean_w, M);
   };
-  __shared__ int s_first[2][NW];
-  __shared__ unsigned char s_L[2][NT], s_R[2][NT];
-  BNBG_PAVA_PROBE(2);
-  int lo = kbar - 1, hi = kbar, buf = 0;
-  bool left_phase = true;
-  for (;;) {
-    bool L = false, R = false, ev;
-    if (left_phase) {  // state t = (lo - t, hi)
-      const int cl = lo - tid;
-      if (cl >= 0) {
-        const Frac pv = pooled_f(cl, hi);
-        L = cl > 0 && less(v_f(cl - 1), pv);
-        R = hi < pf - 1 && less(pv, v_f(hi + 1));
+  // The expansion is replayed by warp 0 alone, 32 consecutive states per
+  // step (no block barrier inside the walk): a left run tests (lo - t, hi),
+  // a right run (lo, hi + t); the first state that ends the run is located
+  // with a ballot, in the reference's decision order (left test first).
+  __shared__ int s_lohi[2];
+  int lo = kbar - 1, hi = kbar;
+  if (warp == 0) {
+    bool left_phase = true;
+    for (;;) {
+      bool L = false, R = false, ev;
+      if (left_phase) {  // state t = (lo - t, hi)
+        const int cl = lo - lane;
+        if (cl >= 0) {
+          const Frac pv = pooled_f(cl, hi);
+          L = cl > 0 && less(v_f(cl - 1), pv);
+          R = hi < pf - 1 && less(pv, v_f(hi + 1));
+        }
+        ev = !L;
+      } else {  // state t = (lo, hi + t)
+        const int ch = hi + lane;
+        if (ch <= pf - 1) {
+          const Frac pv = pooled_f(lo, ch);
+          L = lo > 0 && less(v_f(lo - 1), pv);
+          R = ch < pf - 1 && less(pv, v_f(ch + 1));
+        }
+        ev = L || !R;
       }
-      ev = !L;
-    } else {  // state t = (lo, hi + t)
-      const int ch = hi + tid;
-      if (ch <= pf - 1) {
-        const Frac pv = pooled_f(lo, ch);
-        L = lo > 0 && less(v_f(lo - 1), pv);
-        R = ch < pf - 1 && less(pv, v_f(ch + 1));
+      const unsigned bal = __ballot_sync(0xffffffffu, ev);
+      if (!bal) {
+        if (left_phase)
+          lo -= 32;
+        else
+          hi += 32;
+        continue;
       }
-      ev = L || !R;
+      const int first = __ffs(bal) - 1;
+      const bool Lf = __shfl_sync(0xffffffffu, L, first);
+      const bool Rf = __shfl_sync(0xffffffffu, R, first);
+      if (left_phase) {
+        lo -= first;
+        if (!Rf) break;
+        ++hi;
+        left_phase = false;
+      } else {
+        hi += first;
+        if (!Lf) break;
+        --lo;
+        left_phase = true;
+      }
     }
-    s_L[buf][tid] = L;
-    s_R[buf][tid] = R;
-    const unsigned bal = __ballot_sync(0xffffffffu, ev);
-    if (lane == 0) s_first[buf][warp] = bal ? warp * 32 + __ffs(bal) - 1 : NT;
-    __syncthreads();
-    int first = NT;
-#pragma unroll
-    for (int w2 = 0; w2 < NW; ++w2) first = min(first, s_first[buf][w2]);
-    if (first == NT) {
-      if (left_phase)
-        lo -= NT;
-      else
-        hi += NT;
-      buf ^= 1;
-      continue;
-    }
-    const bool Lf = s_L[buf][first], Rf = s_R[buf][first];
-    buf ^= 1;
-    if (left_phase) {
-      lo -= first;
-      if (!Rf) break;
-      ++hi;
-      left_phase = false;
-    } else {
-      hi += first;
-      if (!Lf) break;
-      --lo;
-      left_phase = true;
+    if (lane == 0) {
+      s_lohi[0] = lo;
+      s_lohi[1] = hi;
     }
   }
+  __syncthreads();
+  lo = s_lohi[0];
+  hi = s_lohi[1];
   blo = lo;
   bhi = hi;
   BNBG_PAVA_PROBE(3);
@@ -371,6 +394,8 @@ struct ColSmem {
   double* scan;
   double* xk;
   int* xi;
+  double* bo;   // p: staged previous iterate B (prox) / beta (eval)
+  uint8_t* st;  // p: staged coordinate states
 };
 __device__ __forceinline__ ColSmem col_smem(double* sm, int p, int n2, int E) {
   const int ns = sort_slots(n2, E);
@@ -381,6 +406,10 @@ __device__ __forceinline__ ColSmem col_smem(double* sm, int p, int n2, int E) {
   c.scan = c.u + p;
   c.xk = c.scan + ns;
   c.xi = reinterpret_cast<int*>(c.xk + 2 * ns);
+  // staged B / states after xk[2 ns] and xi[2 ns]; the shared-memory sort
+  // (E = 0, p > 1024) reads them from global memory instead
+  c.bo = E ? c.xk + 3 * ns : nullptr;
+  c.st = E ? reinterpret_cast<uint8_t*>(c.bo + p) : nullptr;
   return c;
 }
 
@@ -446,35 +475,77 @@ static __global__ void k_init_cols(int p, int m, const uint8_t* state, int* pf, 
 
 // ---------------------------------------------------------------------------
 // VK5: proximal-gradient step + FISTA momentum for every active column.
+//
+// ColCache: a CTA that owns the same column across iterations (the
+// persistent pass kernel, between compactions) keeps the column's B, V and
+// states in shared memory and its scalars in registers, so an iteration only
+// reads the gradient slabs from global memory.  Global B / V / t are still
+// written every iteration (the GEMMs and the evaluation read them).
 // ---------------------------------------------------------------------------
-template <int E>
-__device__ void prox_column(const RelaxDev& r, int c, double* sm) {
-  const int b = r.act[c];
+struct ColCache {
+  int b, kb, pf;
+  double t;
+  double* B;          // p, shared
+  double* V;          // p, shared
+  const uint8_t* st;  // p, shared
+};
+
+template <int E, bool CACHED>
+__device__ __forceinline__ double prox_column_impl(const RelaxDev& r, int ns, int c, double* sm,
+                                                   const ColCache cc0) {
+  const ColCache* cc = &cc0;
+  const int b = CACHED ? cc->b : r.act[c];
   const int p = r.p;
   const ColSmem S = col_smem(sm, p, r.n2, E);
-  const uint8_t* st = r.state + (size_t)b * p;
+  const uint8_t* st = CACHED ? cc->st : r.state + (size_t)b * p;
   double* Vb = r.V + (size_t)b * p;
   double* Bb = r.B + (size_t)b * p;
-  const double tm = r.t[b];
+  const double* Vsrc = CACHED ? cc->V : Vb;
+  const double tm = CACHED ? cc->t : r.t[b];
+  ColProbe pr(r.probe);
   bool bad = false;
   column_sort<kNodeThreads, E>(
       p, r.n2,
       [&](int j) {
-        const double v = Vb[j];
+        const double v = Vsrc[j];
+        const uint8_t sj = st[j];
+        if (E && !CACHED) {
+          S.bo[j] = Bb[j];
+          S.st[j] = sj;
+        }
         bad |= !isfinite(v);
-        const double uj = v - r.eta * gsum(r, b, j);  // U = V - eta G (relaxation.hpp:229)
+        const double uj = v - r.eta * gsum(r, ns, b, j);  // U = V - eta G (relaxation.hpp:229)
         S.u[j] = uj;
-        return st[j] == kFree ? r.rho * fabs(uj) : -1.0;
+        const double key = sj == kFree ? r.rho * fabs(uj) : -1.0;
+        // a NaN key would break the sorting network's order (and the rank ->
+        // index map); the column is reported as numeric_error, so any total
+        // order will do
+        return key == key ? key : -1.0;
       },
       S.key, S.idx, S.xk, S.xi);
   if (bad) atomicMin(r.d_err, b);  // refresh_predictions' finite check (relaxation.hpp:76-81)
-  const int kb = r.kbar[b], pf = r.pf[b];
+  const int kb = CACHED ? cc->kb : r.kbar[b];
+  const int pf = CACHED ? cc->pf : r.pf[b];
+  const double* bo_src = CACHED ? cc->B : (E ? S.bo : Bb);
+  const uint8_t* st_src = CACHED ? cc->st : (E ? S.st : st);
   int lo, hi;
   double pooled;
+  pr.mark(0);
   block_pava<kNodeThreads>(S.key, pf, kb, r.rho, r.M, S.scan, lo, hi, pooled);
+  pr.mark(1);
   const double inv_rho = 1.0 / r.rho;
   const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * tm * tm));
   const double coef = (tm - 1.0) / t_next;
+  auto put = [&](int j, double out) {
+    const double bo = bo_src[j];
+    const double vn = r.accel ? out + coef * (out - bo) : out;
+    Vb[j] = vn;
+    Bb[j] = out;
+    if (CACHED) {
+      cc->V[j] = vn;
+      cc->B[j] = out;
+    }
+  };
   // free coordinates by rank (prox_kernel.hpp:267-275)
   for (int rk = threadIdx.x; rk < pf; rk += kNodeThreads) {
     const int j = S.idx[rk];
@@ -488,29 +559,33 @@ __device__ void prox_column(const RelaxDev& r, int c, double* sm) {
       const double sign = uj > 0.0 ? 1.0 : (uj < 0.0 ? -1.0 : 0.0);
       out = uj - inv_rho * sign * v;
     }
-    const double bo = Bb[j];
-    Vb[j] = r.accel ? out + coef * (out - bo) : out;
-    Bb[j] = out;
+    put(j, out);
   }
   // fixed coordinates (prox_kernel.hpp:261-266)
   for (int j = threadIdx.x; j < p; j += kNodeThreads) {
-    const uint8_t s = st[j];
+    const uint8_t s = st_src[j];
     if (s == kFree) continue;
     const double uj = S.u[j];
     const double out = s == kFixedZero ? 0.0 : uj - inv_rho * d_prox_huber(r.rho * uj, r.rho, r.M);
-    const double bo = Bb[j];
-    Vb[j] = r.accel ? out + coef * (out - bo) : out;
-    Bb[j] = out;
+    put(j, out);
   }
-  if (threadIdx.x == 0 && r.accel) r.t[b] = t_next;
+  if (r.accel && threadIdx.x == 0) r.t[b] = t_next;
+  pr.mark(2);
   __syncthreads();
+  pr.mark(3);
+  return r.accel ? t_next : tm;  // the column's new momentum scalar
+}
+
+template <int E>
+__device__ void prox_column(const RelaxDev& r, int ns, int c, double* sm) {
+  prox_column_impl<E, false>(r, ns, c, sm, ColCache{});
 }
 
 template <int E>
 __global__ void __launch_bounds__(kNodeThreads) k_prox_fista(RelaxDev r) {
   extern __shared__ __align__(16) double sm[];
   if ((int)blockIdx.x >= *r.d_ma) return;
-  prox_column<E>(r, blockIdx.x, sm);
+  prox_column<E>(r, r.nsplit, blockIdx.x, sm);
 }
 
 // ---------------------------------------------------------------------------
@@ -646,40 +721,130 @@ struct EvalArgs {
   int eval_idx;
 };
 
-template <int E>
-__device__ void eval_column(const RelaxDev& r, const EvalArgs& e, int c, double* sm) {
-  const int b = r.act[c];
+// One pass over the column gathers every statistic the bound needs (finite
+// check, g(beta) domain / nonzero / budget sums, g*(Q) Huber sums, the
+// row-block loss and conjugate partials) and reduces them together; only the
+// binding g(beta) case and the TopSum of g*(Q) sort.  With a ColCache the
+// column's B and states come from shared memory.
+template <int E, bool CACHED>
+__device__ void eval_column_impl(const RelaxDev& r, int ns, const EvalArgs& e, int c, double* sm,
+                                 const ColCache cc0) {
+  const ColCache* cc = CACHED ? &cc0 : nullptr;
+  const int b = cc ? cc->b : r.act[c];
   const int p = r.p;
   const ColSmem S = col_smem(sm, p, r.n2, E);
   double* q = S.u;
-  __shared__ double red[kNodeThreads / 32];
-  __shared__ int ired[kNodeThreads / 32];
+  constexpr int NV = 10;
+  __shared__ double red[(kNodeThreads / 32) * NV];
   __shared__ int s_restart;
-  const uint8_t* st = r.state + (size_t)b * p;
-  const double* Bb = r.B + (size_t)b * p;
-
+  const uint8_t* st = cc ? cc->st : r.state + (size_t)b * p;
+  const double* Bb = cc ? cc->B : r.B + (size_t)b * p;
+  const int kb = cc ? cc->kb : r.kbar[b];
   const double inv2l = 1.0 / (2.0 * r.lambda2);
-  bool bad = false;
+  const double M = r.M, box_tol = M * (1.0 + 1e-9);
+  // v: 0 finite-bad, 1 domain-bad, 2 fixed-one sum b^2, 3 free nonzeros, 4 free count,
+  //    5 free sum b^2, 6 sum_{J1} H_M(q), 7 sum_free H_M(q), 8 sum l(S), 9 sum l*(R)
+  double v[NV];
+#pragma unroll
+  for (int t = 0; t < NV; ++t) v[t] = 0.0;
   for (int j = threadIdx.x; j < p; j += kNodeThreads) {
-    bad |= !isfinite(Bb[j]);
-    q[j] = -gsum(r, b, j) * inv2l;  // Z = -R; Q = X'Z; Q *= 1/(2 lambda2)
+    const double bj = Bb[j];
+    const uint8_t sj = st[j];
+    const double qj = -gsum(r, ns, b, j) * inv2l;  // Z = -R; Q = X'Z; Q *= 1/(2 lambda2)
+    q[j] = qj;
+    v[0] += !isfinite(bj) ? 1.0 : 0.0;
+    if (sj == kFixedZero) {
+      v[1] += bj != 0.0 ? 1.0 : 0.0;
+    } else if (sj == kFixedOne) {
+      v[1] += fabs(bj) > box_tol ? 1.0 : 0.0;
+      v[2] += bj * bj;
+      v[6] += d_huber(qj, M);
+    } else {
+      v[1] += fabs(bj) > box_tol ? 1.0 : 0.0;
+      v[3] += bj != 0.0 ? 1.0 : 0.0;
+      v[4] += 1.0;
+      v[5] += bj * bj;
+      v[7] += d_huber(qj, M);
+    }
   }
-  if (bad) atomicMin(r.d_err, b);
-  __syncthreads();
-  const int kb = r.kbar[b];
-  // Phi = sum l(S) + 2 lambda2 g(B)  (relaxation.hpp:108-123)
-  const double g = block_g_value<kNodeThreads, E>(Bb, st, p, r.n2, kb, r.M, S, red, ired);
-  // Psi = -sum l*(R) - 2 lambda2 g*(Q)  (relaxation.hpp:127-147)
-  const double gs = block_g_conj<kNodeThreads, E>(q, st, p, r.n2, kb, r.M, S, red);
+  for (int rb = threadIdx.x; rb < e.nrb; rb += kNodeThreads) {
+    v[8] += e.part_loss[(size_t)rb * e.part_ld + b];
+    v[9] += e.part_conj[(size_t)rb * e.part_ld + b];
+  }
+  block_sum_vec<kNodeThreads, NV>(v, red);
+  if (v[0] != 0.0 && threadIdx.x == 0) atomicMin(r.d_err, b);
+  const int nonzero = (int)v[3], pf = (int)v[4];
+  // g(beta) (prox_kernel.hpp:310-347, recover_core primal_heuristics.hpp:60-99)
+  double g;
+  if (v[1] != 0.0) {
+    g = d_inf();
+  } else if (kb <= 0) {
+    g = nonzero > 0 ? d_inf() : 0.5 * v[2];
+  } else if (nonzero <= kb) {
+    g = 0.5 * (v[2] + v[5]);
+  } else {
+    column_sort<kNodeThreads, E>(
+        p, r.n2, [&](int j) { return st[j] == kFree ? fabs(Bb[j]) : -1.0; }, S.key, S.idx, S.xk,
+        S.xi);
+    const double* key = S.key;
+    double tl = 0.0;  // ranks below kbar
+    for (int rk = kb + threadIdx.x; rk < pf; rk += kNodeThreads) tl += key[rk];
+    const double tail = block_sum<kNodeThreads>(tl, red);
+    __shared__ double s_tau;
+    __shared__ int s_cap, s_ok;
+    if (threadIdx.x == 0) {
+      // smallest s with key[s-1] >= tau_s >= key[s], tau_s = suffix_s / (kbar - s)
+      int ok = 0, cap = 0;
+      double tau = 0.0;
+      // suffix sums accumulated from the bottom, as the reference does
+      // (primal_heuristics.hpp:82-84); kbar <= k is small
+      for (int s2 = 0; s2 < kb; ++s2) {
+        double sf = tail;
+        for (int t = kb - 1; t >= s2; --t) sf += key[t];
+        const double tv = sf / (double)(kb - s2);
+        const double upper = s2 == 0 ? d_inf() : key[s2 - 1];
+        const double lower = key[s2];
+        if (upper >= tv && tv >= lower) {
+          ok = 1;
+          tau = tv;
+          cap = s2;
+          break;
+        }
+      }
+      s_ok = ok && !(tau > M * (1.0 + 1e-9));
+      s_tau = tau;
+      s_cap = cap;
+    }
+    __syncthreads();
+    if (!s_ok) {
+      g = d_inf();
+    } else {
+      const double tau = s_tau;
+      const int cap = s_cap;
+      double fp = 0.0;
+      for (int rk = threadIdx.x; rk < pf; rk += kNodeThreads)
+        fp += rk < cap ? key[rk] * key[rk] : tau * key[rk];
+      g = 0.5 * (v[2] + block_sum<kNodeThreads>(fp, red));
+    }
+  }
+  // g*(Q): sum_{J1} H_M(q) + TopSum_kbar over free H_M(q) (prox_kernel.hpp:351-370)
+  double gs;
+  if (kb <= 0) {
+    gs = v[6];
+  } else if (pf <= kb) {
+    gs = v[6] + v[7];
+  } else {
+    column_sort<kNodeThreads, E>(
+        p, r.n2, [&](int j) { return st[j] == kFree ? d_huber(q[j], M) : -1.0; }, S.key, S.idx,
+        S.xk, S.xi);
+    double s2 = 0.0;
+    for (int rk = threadIdx.x; rk < kb; rk += kNodeThreads) s2 += S.key[rk];
+    gs = v[6] + block_sum<kNodeThreads>(s2, red);
+  }
   if (threadIdx.x == 0) {
     s_restart = 0;
-    double loss = 0.0, conj = 0.0;
-    for (int rb = 0; rb < e.nrb; ++rb) {
-      loss += e.part_loss[(size_t)rb * e.part_ld + b];
-      conj += e.part_conj[(size_t)rb * e.part_ld + b];
-    }
-    const double phi = loss + 2.0 * r.lambda2 * g;
-    const double psi = -conj - 2.0 * r.lambda2 * gs;
+    const double phi = v[8] + 2.0 * r.lambda2 * g;      // relaxation.hpp:108-123
+    const double psi = -v[9] - 2.0 * r.lambda2 * gs;    // relaxation.hpp:127-147
     double best = r.best[b];
     if (psi > best) best = psi;
     r.best[b] = best;
@@ -708,10 +873,15 @@ __device__ void eval_column(const RelaxDev& r, const EvalArgs& e, int c, double*
 }
 
 template <int E>
+__device__ void eval_column(const RelaxDev& r, int ns, const EvalArgs& e, int c, double* sm) {
+  eval_column_impl<E, false>(r, ns, e, c, sm, ColCache{});
+}
+
+template <int E>
 __global__ void __launch_bounds__(kNodeThreads) k_eval(RelaxDev r, EvalArgs e) {
   extern __shared__ __align__(16) double sm[];
   if ((int)blockIdx.x >= *r.d_ma) return;
-  eval_column<E>(r, e, blockIdx.x, sm);
+  eval_column<E>(r, r.nsplit, e, blockIdx.x, sm);
 }
 
 // order-preserving compaction of the active list by one CTA of NT threads
@@ -803,8 +973,12 @@ __global__ void __launch_bounds__(kNodeThreads)
   for (int j = threadIdx.x; j < p; j += kNodeThreads) cnt += st[j] == kFree;
   const int pf = (int)block_sum<kNodeThreads>((double)cnt, red);
   column_sort<kNodeThreads, E>(
-      p, n2, [&](int j) { return st[j] == kFree ? scale * fabs(u[j]) : -1.0; }, S.key, S.idx,
-      S.xk, S.xi);
+      p, n2,
+      [&](int j) {
+        const double key = st[j] == kFree ? scale * fabs(u[j]) : -1.0;
+        return key == key ? key : -1.0;
+      },
+      S.key, S.idx, S.xk, S.xi);
   const int kb = kbar[b];
   int lo, hi;
   double pooled;

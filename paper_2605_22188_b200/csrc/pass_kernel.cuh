@@ -7,18 +7,30 @@
 // ramp/drain per step and a host round trip per check interval.  Here one
 // CTA per SM loops over the iterations on the device:
 //
-//   phase NN   row tiles of X (BM=16) x active columns     -> R = l'(X V)
-//   grid.sync
+//   phase NN   row tiles of X x active columns           -> R = l'(X V)
+//   grid barrier
 //   phase TN   column tiles of X x active columns x split-K -> G slabs
-//   grid.sync
+//   grid barrier
 //   phase prox one CTA per active column                  -> B, V
-//   grid.sync
+//   grid barrier
 //   every check_interval: NN(eval) / TN / per-column bounds / compaction,
 //   with the active count read back on the device (no host round trip).
 //
-// The per-phase code is exactly the standalone kernels' (gemm_tile,
-// prox_column, eval_column, compact_active), so results are identical to the
-// multi-kernel path; only the scheduling differs.
+// Two operand modes:
+//   resident (ResLayout.on): when X fits in the SMs' shared memory (c1, c2:
+//     8 MB over 148 x 227 KB), CTA b loads its NN row tile and its TN tile of
+//     X once per pass and keeps them for every iteration; an iteration then
+//     only moves V / R chunks (cp.async, all k at once) and the DMMA fragments
+//     come straight from shared memory.
+//   streaming: X tiles are staged through a cp.async ring per iteration
+//     (gemm_tile, the standalone kernels' code) -- c3/c4 sizes.
+//
+// The grid barrier is a monotone arrival counter: CTA leaders add with
+// red.release.gpu and poll with ld.acquire.gpu until the epoch target, one
+// L2 round trip less than an atomic-return barrier.
+//
+// The column phases (prox_column, eval_column, compact_active) are the
+// standalone kernels' code, so results do not depend on the scheduling mode.
 #pragma once
 #include <cooperative_groups.h>
 
@@ -28,18 +40,33 @@
 
 namespace bnbg {
 
-namespace cg = cooperative_groups;
-
 constexpr int kPassThreads = kNodeThreads;  // 8 warps
 constexpr int kPassNW = kPassThreads / 32;
 
 __device__ __forceinline__ int pass_fn(int ma) { return ma <= 8 ? 1 : (ma <= 16 ? 2 : 4); }
 
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target) {
+  target += gridDim.x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ctr) : "memory");
+    } while ((int)(v - target) < 0);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// streaming-mode phases
+// ---------------------------------------------------------------------------
 template <int EPI>
 __device__ void pass_phase_nn(const PassArgs& a, const double* Bsrc, int ma, double* smem,
-                              int* colmap) {
+                              int* colmap, const int* act) {
   GemmArgs g = a.nn;
   g.B = Bsrc;
+  g.act = act;
   const int fn = pass_fn(ma);
   const int mt = (a.n + 15) / 16;
   const int nt = (ma + 8 * fn - 1) / (8 * fn);
@@ -55,8 +82,10 @@ __device__ void pass_phase_nn(const PassArgs& a, const double* Bsrc, int ma, dou
 }
 
 // returns the split-K factor used (the consumers sum that many slabs)
-__device__ inline int pass_phase_tn(const PassArgs& a, int ma, double* smem, int* colmap) {
+__device__ inline int pass_phase_tn(const PassArgs& a, int ma, double* smem, int* colmap,
+                                    const int* act) {
   GemmArgs g = a.tn;
+  g.act = act;
   const int fn = pass_fn(ma);
   const int mt = (a.p + 15) / 16;
   const int nt = (ma + 8 * fn - 1) / (8 * fn);
@@ -81,7 +110,7 @@ __device__ inline int pass_phase_tn(const PassArgs& a, int ma, double* smem, int
   return nsplit;
 }
 
-// dynamic shared memory of k_pass
+// dynamic shared memory of the streaming-mode k_pass
 __host__ inline size_t pass_smem_bytes(int p, int n2, int E) {
   size_t b = column_smem_bytes(p, n2, E);
   const size_t g1 = GemmShape<false, 2, 4, kPassNW>::SMEM_BYTES;
@@ -91,40 +120,327 @@ __host__ inline size_t pass_smem_bytes(int p, int n2, int E) {
   return b;
 }
 
+// ---------------------------------------------------------------------------
+// resident mode
+// ---------------------------------------------------------------------------
+constexpr int kResBM = 16;  // FM = 2
+
+__host__ __device__ inline int ld_mod16_4(int v) {  // smallest >= v with (x % 16) == 4
+  int x = (v + 3) & ~3;
+  while (x % 16 != 4) x += 4;
+  return x;
+}
+
+// work region: staged B chunk (up to 16 columns x ldb), reused afterwards for
+// the cross-warp reduction (NW x 2 x FN x 64) and the l / l* staging (2 x 16 x 16)
+__host__ __device__ inline size_t res_work_doubles(const ResLayout& r) {
+  size_t b = (size_t)16 * r.ldb;
+  const size_t red = (size_t)kPassNW * 2 * 2 * 64 + 2 * 16 * 16;
+  return b > red ? b : red;
+}
+
+// Loads this CTA's resident tiles of X (once per pass).
+__device__ void res_load_x(const PassArgs& a, double* smem) {
+  const ResLayout& L = a.res;
+  const double* X = a.nn.A;
+  const int n = a.n, p = a.p;
+  if ((int)blockIdx.x < L.nn_tiles) {
+    const int m0 = blockIdx.x * kResBM;
+    double* A = smem;
+    for (int e = threadIdx.x; e < L.kpad_nn * kResBM; e += kPassThreads) {
+      const int k = e / kResBM, m = e % kResBM;
+      A[k * L.lda_nn + m] = (k < p && m0 + m < n) ? X[(size_t)k * n + m0 + m] : 0.0;
+    }
+  }
+  if ((int)blockIdx.x < L.tn_mt * L.tn_split) {
+    const int i = blockIdx.x % L.tn_mt, sp = blockIdx.x / L.tn_mt;
+    const int c0 = i * kResBM, r0 = sp * L.tn_klen;
+    double* A = smem + L.off_tn;
+    for (int e = threadIdx.x; e < kResBM * L.tn_klen; e += kPassThreads) {
+      const int m = e / L.tn_klen, k = e % L.tn_klen;
+      const int row = r0 + k;
+      A[m * L.ldk_tn + k] = (c0 + m < p && row < n) ? X[(size_t)(c0 + m) * n + row] : 0.0;
+    }
+  }
+  __syncthreads();
+}
+
+// One output tile (16 rows x 8*FN compact columns starting at n0) from the
+// resident A operand: NN  A[k*lda + m] (K = kpad_nn), TN  A[m*lda + k] (K = tn_klen).
+// B chunk: column c at g.B + col*g.ldb + kbeg, kvalid valid rows (rest zero).
+template <bool TN, int FN, int EPI>
+__device__ void res_tile(const GemmArgs& g, const double* Ares, int lda, int K, int kbeg,
+                         int kvalid, int m0, int mt, int n0, int ncols, int split, double* work,
+                         int ldb, int* colmap) {
+  constexpr int FM = 2, BM = 16, BN = 8 * FN, NW = kPassNW, NT = kPassThreads;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  ColProbe pr(g.probe);
+  if (tid < BN) {
+    const int c = n0 + tid;
+    colmap[tid] = c < ncols ? (g.act ? g.act[c] : c) : -1;
+  }
+  __syncthreads();
+  double* Bs = work;
+  // B chunk: 16-byte copies when the rows are 16-byte aligned (even ld and
+  // offset), else 8-byte; rows past kvalid are zero-filled
+  if (((g.ldb | kbeg) & 1) == 0 && ((reinterpret_cast<size_t>(g.B) & 15) == 0)) {
+    const int K2 = K >> 1;
+    for (int e = tid; e < BN * K2; e += NT) {
+      const int c = e / K2, k = 2 * (e - c * K2);
+      const int col = colmap[c];
+      const int nb = col < 0 ? 0 : (k + 2 <= kvalid ? 16 : (k < kvalid ? 8 : 0));
+      cp_async_16(Bs + c * ldb + k, nb ? g.B + (size_t)col * g.ldb + kbeg + k : g.B, nb);
+    }
+  } else {
+    for (int c = 0; c < BN; ++c) {
+      const int col = colmap[c];
+      const double* src = col >= 0 ? g.B + (size_t)col * g.ldb + kbeg : g.B;
+      for (int k = tid; k < K; k += NT) {
+        const bool valid = col >= 0 && k < kvalid;
+        cp_async_8(Bs + c * ldb + k, valid ? src + k : g.B, valid);
+      }
+    }
+  }
+  cp_async_commit();
+  pr.mark(0);
+  cp_async_wait<0>();
+  __syncthreads();
+  pr.mark(1);
+  // two accumulator sets (even / odd k-steps of the warp) halve the DMMA
+  // dependency chain; they are added in a fixed order afterwards
+  double acc[2][FM][FN][2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j) acc[u][i][j][0] = acc[u][i][j][1] = 0.0;
+  const int nks = K >> 2;
+  auto kstep = [&](int u, int ks) {
+    const int kk = ks * 4 + (lane & 3);
+    double av[FM], bv[FN];
+#pragma unroll
+    for (int i = 0; i < FM; ++i) {
+      const int row = i * 8 + (lane >> 2);
+      av[i] = TN ? Ares[row * lda + kk] : Ares[kk * lda + row];
+    }
+#pragma unroll
+    for (int j = 0; j < FN; ++j) bv[j] = Bs[(j * 8 + (lane >> 2)) * ldb + kk];
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j) dmma_8x8x4(acc[u][i][j][0], acc[u][i][j][1], av[i], bv[j]);
+  };
+  int ks = warp;
+  for (; ks + NW < nks; ks += 2 * NW) {
+    kstep(0, ks);
+    kstep(1, ks + NW);
+  }
+  if (ks < nks) kstep(0, ks);
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) {
+      acc[0][i][j][0] += acc[1][i][j][0];
+      acc[0][i][j][1] += acc[1][i][j][1];
+    }
+  __syncthreads();  // Bs consumed: the work region becomes the reduction buffer
+  pr.mark(2);
+  double* red = work;
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) red[((warp * FM + i) * FN + j) * 64 + h * 32 + lane] = acc[0][i][j][h];
+  __syncthreads();
+  double* lv = work + NW * FM * 2 * 64;
+  double* cv = lv + BM * BN;
+  double* Cout = g.C + (size_t)split * g.split_stride;
+  for (int e = tid; e < BM * BN; e += NT) {
+    const int c = e / BM, r = e % BM;
+    const int i = r >> 3, j = c >> 3;
+    const int ln = (r & 7) * 4 + ((c & 7) >> 1), h = c & 1;
+    const int off = (i * FN + j) * 64 + h * 32 + ln;
+    constexpr int stride_w = FM * FN * 64;
+    double s = red[off];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) s += red[off + w * stride_w];
+    const int gm = m0 + r;
+    const int col = colmap[c];
+    if (EPI == EPI_STORE) {
+      if (gm < g.M && col >= 0) Cout[(size_t)col * g.ldc + gm] = s;
+    } else {
+      double rv = 0.0, l = 0.0, cj = 0.0;
+      if (gm < g.M && col >= 0) {
+        const double yv = g.y[gm];
+        rv = d_loss_deriv(g.loss, s, yv);
+        Cout[(size_t)col * g.ldc + gm] = rv;
+        if (EPI == EPI_EVAL) {
+          l = d_loss_value(g.loss, s, yv);
+          cj = d_loss_conj(g.loss, rv, yv);
+        }
+      }
+      if (EPI == EPI_EVAL) {
+        lv[c * BM + r] = l;
+        cv[c * BM + r] = cj;
+      }
+    }
+  }
+  if (EPI == EPI_EVAL) {
+    __syncthreads();
+    if (tid < BN && colmap[tid] >= 0) {
+      double sl = 0.0, sc = 0.0;
+      for (int r = 0; r < BM; ++r) {
+        sl += lv[tid * BM + r];
+        sc += cv[tid * BM + r];
+      }
+      g.part_loss[(size_t)mt * g.part_ld + colmap[tid]] = sl;
+      g.part_conj[(size_t)mt * g.part_ld + colmap[tid]] = sc;
+    }
+  }
+  __syncthreads();
+  pr.mark(3);
+}
+
+template <int EPI>
+__device__ void res_phase_nn(const PassArgs& a, const double* Bsrc, int ma, double* smem,
+                             int* colmap, const int* act) {
+  const ResLayout& L = a.res;
+  if ((int)blockIdx.x >= L.nn_tiles) return;
+  GemmArgs g = a.nn;
+  g.B = Bsrc;
+  g.act = act;
+  double* work = smem + L.off_work;
+  const int m0 = blockIdx.x * kResBM;
+  for (int n0 = 0; n0 < ma; n0 += 16) {
+    if (ma - n0 > 8)
+      res_tile<false, 2, EPI>(g, smem, L.lda_nn, L.kpad_nn, 0, a.p, m0, blockIdx.x, n0, ma, 0,
+                              work, L.ldb, colmap);
+    else
+      res_tile<false, 1, EPI>(g, smem, L.lda_nn, L.kpad_nn, 0, a.p, m0, blockIdx.x, n0, ma, 0,
+                              work, L.ldb, colmap);
+  }
+}
+
+__device__ void res_phase_tn(const PassArgs& a, int ma, double* smem, int* colmap,
+                             const int* act) {
+  const ResLayout& L = a.res;
+  if ((int)blockIdx.x >= L.tn_mt * L.tn_split) return;
+  GemmArgs g = a.tn;
+  g.act = act;
+  double* work = smem + L.off_work;
+  const int i = blockIdx.x % L.tn_mt, sp = blockIdx.x / L.tn_mt;
+  const int r0 = sp * L.tn_klen;
+  const int kvalid = min(L.tn_klen, a.n - r0);
+  for (int n0 = 0; n0 < ma; n0 += 16) {
+    if (ma - n0 > 8)
+      res_tile<true, 2, EPI_STORE>(g, smem + L.off_tn, L.ldk_tn, L.tn_klen, r0, kvalid,
+                                   i * kResBM, i, n0, ma, sp, work, L.ldb, colmap);
+    else
+      res_tile<true, 1, EPI_STORE>(g, smem + L.off_tn, L.ldk_tn, L.tn_klen, r0, kvalid,
+                                   i * kResBM, i, n0, ma, sp, work, L.ldb, colmap);
+  }
+}
+
 __device__ __forceinline__ unsigned long long pass_clock() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
 
-// phase wall-time accumulation (tools/profile_solve.py; off in the product)
+// phase wall-time accumulation (tools/pass_phases.py; off in the product)
 enum { PH_NN = 0, PH_TN, PH_PROX, PH_EVNN, PH_EVTN, PH_EVCOL, PH_COMPACT, PH_COUNT };
 
+constexpr int kActCache = 256;
+
 template <int E>
-__global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a) {
+__global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant__ PassArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int colmap[32];
-  cg::grid_group grid = cg::this_grid();
-  RelaxDev r = a.r;
+  __shared__ int s_act[kActCache];  // the active list, refreshed after every compaction
+  const RelaxDev& r = a.r;  // kernel-parameter space (no local copy)
+  int nsplit = 1;            // split-K slabs of the current G
+  const bool res = a.res.on != 0;
+  double* colsm = res ? smem + a.res.off_work : smem;  // column phases' shared memory
   int iter = 0, last_eval = 0, n_evals = 0;
   long long node_its = 0;
-  int ma = *(volatile int*)r.d_ma;
+  unsigned bar_target = 0;
+  if (res) res_load_x(a, smem);
+  int ma = 0;
+  const int* actp = r.act;
+  // CTA c owns active column c between compactions: its B, V, states in
+  // shared memory (ColCache), refreshed from global after every evaluation
+  ColCache cc;
+  bool cached = false;
+  const bool can_cache = res && E != 0 && a.res.off_cc > 0;
+  auto refresh = [&]() {
+    ma = *(volatile int*)r.d_ma;
+    for (int i = threadIdx.x; i < ma && i < kActCache; i += kPassThreads) s_act[i] = r.act[i];
+    __syncthreads();
+    actp = ma <= kActCache ? s_act : r.act;
+    cached = can_cache && ma <= (int)gridDim.x && (int)blockIdx.x < ma;
+    if (cached) {
+      const int p = r.p;
+      const int b = actp[blockIdx.x];
+      cc.b = b;
+      cc.kb = r.kbar[b];
+      cc.pf = r.pf[b];
+      cc.t = r.t[b];
+      cc.B = smem + a.res.off_cc;
+      cc.V = cc.B + p;
+      uint8_t* stc = reinterpret_cast<uint8_t*>(cc.V + p);
+      cc.st = stc;
+      for (int j = threadIdx.x; j < p; j += kPassThreads) {
+        cc.B[j] = r.B[(size_t)b * p + j];
+        cc.V[j] = r.V[(size_t)b * p + j];
+        stc[j] = r.state[(size_t)b * p + j];
+      }
+      __syncthreads();
+    }
+  };
+  refresh();
   const bool prof = a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
   unsigned long long t_last = prof ? pass_clock() : 0ull;
-  auto mark = [&](int ph) {
+  auto mark = [&](int ph) {  // phase end (after its grid barrier)
     if (prof) {
       const unsigned long long t = pass_clock();
       a.prof[ph] += t - t_last;
       t_last = t;
     }
   };
+  auto arrive = [&](int ph) {  // CTA 0 reaches the phase's barrier
+    if (prof) a.prof[8 + ph] += pass_clock() - t_last;
+  };
+  auto phase_nn = [&](const double* src, bool eval) {
+    if (res) {
+      if (eval)
+        res_phase_nn<EPI_EVAL>(a, src, ma, smem, colmap, actp);
+      else
+        res_phase_nn<EPI_DERIV>(a, src, ma, smem, colmap, actp);
+    } else {
+      if (eval)
+        pass_phase_nn<EPI_EVAL>(a, src, ma, smem, colmap, actp);
+      else
+        pass_phase_nn<EPI_DERIV>(a, src, ma, smem, colmap, actp);
+    }
+  };
+  auto phase_tn = [&]() {
+    if (res) {
+      res_phase_tn(a, ma, smem, colmap, actp);
+      return a.res.tn_split;
+    }
+    return pass_phase_tn(a, ma, smem, colmap, actp);
+  };
 
   auto evaluate = [&](int it) {  // relaxation.hpp:194-221
-    pass_phase_nn<EPI_EVAL>(a, r.B, ma, smem, colmap);
-    grid.sync();
+    phase_nn(r.B, true);
+    arrive(PH_EVNN);
+    grid_barrier(a.bar, bar_target);
     mark(PH_EVNN);
-    r.nsplit = pass_phase_tn(a, ma, smem, colmap);
-    grid.sync();
+    nsplit = phase_tn();
+    arrive(PH_EVTN);
+    grid_barrier(a.bar, bar_target);
     mark(PH_EVTN);
     EvalArgs e;
     e.part_loss = a.nn.part_loss;
@@ -136,13 +452,18 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a) {
     e.gap_tolerance = a.gap_tol;
     e.trace = a.trace;
     e.eval_idx = n_evals;
-    for (int c = blockIdx.x; c < ma; c += gridDim.x) eval_column<E>(r, e, c, smem);
-    grid.sync();
+    if (cached)
+      eval_column_impl<E, true>(r, nsplit, e, blockIdx.x, colsm, cc);
+    else
+      for (int c = blockIdx.x; c < ma; c += gridDim.x) eval_column<E>(r, nsplit, e, c, colsm);
+    arrive(PH_EVCOL);
+    grid_barrier(a.bar, bar_target);
     mark(PH_EVCOL);
     if (blockIdx.x == 0) compact_active<kPassThreads>(r.act, r.d_ma, r.frozen);
-    grid.sync();
+    arrive(PH_COMPACT);
+    grid_barrier(a.bar, bar_target);
     mark(PH_COMPACT);
-    ma = *(volatile int*)r.d_ma;
+    refresh();
     // non-finite iterate (numeric_error, relaxation.hpp:76-81): stop early;
     // the host reports the column from d_err
     if (*(volatile int*)r.d_err != 0x7fffffff) ma = 0;
@@ -151,14 +472,20 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a) {
 
   while (iter < a.max_it && ma > 0) {  // relaxation.hpp:224-249
     ++iter;
-    pass_phase_nn<EPI_DERIV>(a, r.V, ma, smem, colmap);
-    grid.sync();
+    phase_nn(r.V, false);
+    arrive(PH_NN);
+    grid_barrier(a.bar, bar_target);
     mark(PH_NN);
-    r.nsplit = pass_phase_tn(a, ma, smem, colmap);
-    grid.sync();
+    nsplit = phase_tn();
+    arrive(PH_TN);
+    grid_barrier(a.bar, bar_target);
     mark(PH_TN);
-    for (int c = blockIdx.x; c < ma; c += gridDim.x) prox_column<E>(r, c, smem);
-    grid.sync();
+    if (cached)
+      cc.t = prox_column_impl<E, true>(r, nsplit, blockIdx.x, colsm, cc);
+    else
+      for (int c = blockIdx.x; c < ma; c += gridDim.x) prox_column<E>(r, nsplit, c, colsm);
+    arrive(PH_PROX);
+    grid_barrier(a.bar, bar_target);
     mark(PH_PROX);
     node_its += ma;
     if (iter % a.check == 0) {

@@ -37,7 +37,21 @@ with P.Engine(inst) as eng:
     tot = 0.0
     for ph in after:
         ms = after[ph] - before.get(ph, 0.0)
-        tot += ms
-        per = ms / its * 1e3 if ph in ("xv", "xtr", "prox") else ms / evals * 1e3
-        print(f"  phase {ph:10s} {ms:9.3f} ms  {per:8.2f} us per {'iteration' if ph in ('xv', 'xtr', 'prox') else 'evaluation'}")
+        tot += 0.0 if ph.endswith("_work") else ms
+        if ph.endswith("_work"):
+            continue
+        w = after.get(ph + "_work", 0.0) - before.get(ph + "_work", 0.0)
+        cnt = its if ph in ("xv", "xtr", "prox") else evals
+        print(f"  phase {ph:10s} {ms:9.3f} ms  {ms / cnt * 1e3:8.2f} us per "
+              f"{'iteration' if cnt == its else 'evaluation'}  (CTA 0 work {w / cnt * 1e3:6.2f} us, "
+              f"barrier wait {(ms - w) / cnt * 1e3:6.2f} us)")
     print(f"  phases total {tot:.3f} ms")
+    raw = eng.pass_profile_raw()
+    its_all = max(1, its)
+    names = ("load+sort", "pava", "scatter", "end barrier")
+    print("  prox sub-phases (CTA 0, per iteration): " +
+          ", ".join(f"{nm} {raw[16 + i] / its_all / 1e3 / 2:.2f} us" for i, nm in enumerate(names)))
+    tn = ("colmap+issue", "load wait", "mma", "reduce+epilogue")
+    for nm, base in (("NN", 20), ("TN", 24)):
+        print(f"  {nm} resident tile sub-phases (CTA 0, per iteration incl. evals): " +
+              ", ".join(f"{t} {raw[base + i] / its_all / 1e3 / 2:.2f} us" for i, t in enumerate(tn)))
