@@ -49,88 +49,60 @@ int set_err(bnbg_handle* h, int code, const std::string& msg) {
   return code;
 }
 
-// ---- node_model.hpp:22-172 ------------------------------------------------
-struct Node {
-  std::vector<int> j0, j1;  // construction order
-  std::vector<double> warm;
-  double lb = -kInf;
-  int depth = 0;
-  bool is_leaf(int k, int p) const {  // node_model.hpp:33-36
-    return k - (int)j1.size() <= 0 || (int)(j0.size() + j1.size()) >= p;
+// ---- node_model.hpp:114-172 -------------------------------------------------
+// Open nodes live in the engine's device-resident pool (pool_kernels.cuh); the
+// best-bound queue holds (lower bound, insertion sequence, pool slot) only.
+// Ties on the bound pop in insertion order (FIFO), as in the reference.
+struct QEntry {
+  double bound;
+  uint64_t seq;
+  int slot;
+  bool operator>(const QEntry& o) const {
+    if (bound != o.bound) return bound > o.bound;
+    return seq > o.seq;
   }
 };
 
-void node_states(const Node& nd, int p, std::vector<uint8_t>& st) {  // :40-45
-  st.assign(p, BNBG_FREE);
-  for (int j : nd.j0) st[j] = BNBG_FIXED_ZERO;
-  for (int j : nd.j1) st[j] = BNBG_FIXED_ONE;
-}
-
-void restore_budget(Node& nd, int k, double M, int p, std::vector<uint8_t>& st) {  // :57-68
-  const int kb = k - (int)nd.j1.size();
-  node_states(nd, p, st);
-  double sum = 0.0;
-  for (int j = 0; j < p; ++j)
-    if (st[j] == BNBG_FREE) sum += std::fabs(nd.warm[j]);
-  const double budget = static_cast<double>(kb) * M;
-  if (sum <= budget) return;
-  const double scale = budget / sum * (1.0 - 1e-12);
-  for (int j = 0; j < p; ++j)
-    if (st[j] == BNBG_FREE) nd.warm[j] *= scale;
-}
-
-// node_model.hpp:77-105
-void branch(const Node& nd, int j, const double* beta, int k, double M, int p, Node& c0, Node& c1,
-            std::vector<uint8_t>& st, std::vector<uint8_t>& st2) {
-  node_states(nd, p, st);
-  c0 = nd;
-  c0.j0.push_back(j);
-  c0.warm.assign(beta, beta + p);
-  c0.warm[j] = 0.0;
-  c0.depth = nd.depth + 1;
-  restore_budget(c0, k, M, p, st2);
-  c1 = nd;
-  c1.j1.push_back(j);
-  c1.warm.assign(beta, beta + p);
-  c1.depth = nd.depth + 1;
-  if (k - (int)c1.j1.size() <= 0) {
-    for (int r = 0; r < p; ++r) {
-      if (r != j && st[r] == BNBG_FREE) {
-        c1.j0.push_back(r);
-        c1.warm[r] = 0.0;
-      }
-    }
-  }
-  restore_budget(c1, k, M, p, st2);
-}
-
-// best-bound queue with FIFO tie-break (node_model.hpp:114-148)
 class NodeQueue {
  public:
-  void push(Node nd) {
-    const double b = nd.lb;
-    heap_.push(Entry{b, seq_++, std::make_shared<Node>(std::move(nd))});
-  }
+  void push(double lb, int slot) { heap_.push(QEntry{lb, seq_++, slot}); }
   bool empty() const { return heap_.empty(); }
   double global_lb() const { return heap_.empty() ? kInf : heap_.top().bound; }
-  Node pop() {
-    Entry e = heap_.top();
+  QEntry pop() {
+    QEntry e = heap_.top();
     heap_.pop();
-    return std::move(*e.node);
+    return e;
   }
 
  private:
-  struct Entry {
-    double bound;
-    uint64_t seq;
-    std::shared_ptr<Node> node;
-    bool operator>(const Entry& o) const {
-      if (bound != o.bound) return bound > o.bound;
-      return seq > o.seq;
-    }
-  };
-  std::priority_queue<Entry, std::vector<Entry>, std::greater<Entry>> heap_;
+  std::priority_queue<QEntry, std::vector<QEntry>, std::greater<QEntry>> heap_;
   uint64_t seq_ = 0;
+};
+
+// A leaf (kbar <= 0 or no free coordinate, node_model.hpp:33-36) skips the
+// relaxation: only its fixed-in support and bound are needed (bnb_engine.hpp:164-175, :200).
+struct Leaf {
+  double lb;
+  std::vector<int> j1;
+};
+
+// Pool slot allocator (host side of the device pool).
+class SlotAllocator {
+ public:
+  int take() {
+    if (!free_.empty()) {
+      const int s = free_.back();
+      free_.pop_back();
+      return s;
+    }
+    return next_++;
+  }
+  void give(int s) { free_.push_back(s); }
+  int high_water() const { return next_; }
+
+ private:
+  std::vector<int> free_;
+  int next_ = 0;
 };
 
 // ---- search policies: solve (bnb_engine.hpp:304-307), rashomon (:169-196)
@@ -243,20 +215,21 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
   cert->batch_size_used = batch_size;
 
   NodeQueue queue;
+  SlotAllocator slots;
   {
-    Node root;  // node_model.hpp:47-52
-    root.warm.assign(p, 0.0);
-    queue.push(std::move(root));
+    const int root = slots.take();  // root_node (node_model.hpp:47-52)
+    if (int rc = eng.pool_root(root)) return set_err(h, rc, eng.err);
+    queue.push(-kInf, root);
   }
-  std::vector<Node> pending;
+  std::vector<Leaf> pending;
   double inc_obj = kInf;
   std::vector<int> inc_sup;
   std::vector<double> inc_coef;
   int status = BNBG_STATUS_OPTIMAL;
-  std::vector<uint8_t> st, st2;
-  std::vector<double> warm;
-  bnbg::BatchLists lists;
   bnbg::PassResult pr;
+  std::vector<int> batch_slots, n01, j0s, j1s, child_slots, rec;
+  std::vector<double> batch_lb, rec_lb;
+  const int kk = std::max(k, 1);
 
   while (!queue.empty() || !pending.empty()) {
     if (elapsed() > cfg.time_limit) {
@@ -264,56 +237,38 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
       break;
     }
     const double threshold = pol.threshold(inc_obj);
-    std::vector<Node> relax_nodes, leaves;
+    std::vector<Leaf> leaves;
     {
       Timer t(cert->transfer_seconds);
       int popped = 0, discarded = 0;  // assemble_batch node_model.hpp:158-172
-      std::vector<Node> batch;
+      batch_slots.clear();
+      batch_lb.clear();
       while (!queue.empty() && popped < batch_size) {
-        Node nd = queue.pop();
-        if (nd.lb >= threshold) {
+        const QEntry e = queue.pop();
+        if (e.bound >= threshold) {
           ++discarded;
+          slots.give(e.slot);
           continue;
         }
-        batch.push_back(std::move(nd));
+        batch_slots.push_back(e.slot);
+        batch_lb.push_back(e.bound);
         ++popped;
       }
       cert->nodes_processed += popped + discarded;
-      for (Node& leaf : pending) {
+      for (Leaf& leaf : pending) {
         ++cert->nodes_processed;
         if (leaf.lb >= threshold) continue;
         leaves.push_back(std::move(leaf));
       }
       pending.clear();
-      for (Node& nd : batch) {
-        if (nd.is_leaf(k, p))
-          leaves.push_back(std::move(nd));
-        else
-          relax_nodes.push_back(std::move(nd));
-      }
-      // pack the batch as CSR lists + warm block (the device packer expands it)
-      const int m = (int)relax_nodes.size();
-      lists.m = m;
-      lists.z_off.assign(m + 1, 0);
-      lists.o_off.assign(m + 1, 0);
-      lists.z_idx.clear();
-      lists.o_idx.clear();
-      warm.resize((size_t)p * m);
-      for (int b = 0; b < m; ++b) {
-        const Node& nd = relax_nodes[b];
-        lists.z_idx.insert(lists.z_idx.end(), nd.j0.begin(), nd.j0.end());
-        lists.o_idx.insert(lists.o_idx.end(), nd.j1.begin(), nd.j1.end());
-        lists.z_off[b + 1] = (int)lists.z_idx.size();
-        lists.o_off[b + 1] = (int)lists.o_idx.size();
-        std::memcpy(warm.data() + (size_t)b * p, nd.warm.data(), sizeof(double) * p);
-      }
     }
-    if (relax_nodes.empty() && leaves.empty()) continue;
+    const int m = (int)batch_slots.size();
+    if (m == 0 && leaves.empty()) continue;
 
-    const int m = (int)relax_nodes.size();
     if (m > 0) {
       Timer t(cert->lower_bound_seconds);
-      const int rc = eng.relax_lists(lists, warm.data(), rp, threshold, on_dual != nullptr, pr);
+      const int rc = eng.relax_pool(m, batch_slots.data(), rp, threshold, on_dual != nullptr, pr,
+                                    on_dual != nullptr, &n01, &j0s, &j1s);
       if (rc) return set_err(h, rc, eng.err);
       ++cert->lb_batches;
       cert->relax_iterations += pr.iterations;
@@ -323,8 +278,8 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
           for (int b = 0; b < m; ++b) {
             const double psi = pr.trace[(size_t)e * m + b];
             if (std::isnan(psi)) continue;
-            const Node& nd = relax_nodes[b];
-            on_dual(user, (int)nd.j0.size(), nd.j0.data(), (int)nd.j1.size(), nd.j1.data(), psi);
+            on_dual(user, n01[2 * b], j0s.data() + (size_t)b * p, n01[2 * b + 1],
+                    j1s.data() + (size_t)b * kk, psi);
           }
       }
     }
@@ -333,13 +288,13 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
     std::vector<int> offsets(1, 0), sidx;
     {
       Timer t(cert->reoptimization_seconds);
-      for (const Node& leaf : leaves) {
+      for (const Leaf& leaf : leaves) {
         sidx.insert(sidx.end(), leaf.j1.begin(), leaf.j1.end());
         offsets.push_back((int)sidx.size());
       }
       for (int b = 0; b < m; ++b) {
         if (pr.status[b] == BNBG_PRUNABLE) continue;
-        const int* row = pr.sup.data() + (size_t)b * std::max(k, 1);
+        const int* row = pr.sup.data() + (size_t)b * kk;
         sidx.insert(sidx.end(), row, row + pr.len[b]);
         offsets.push_back((int)sidx.size());
       }
@@ -374,27 +329,34 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
         }
       }
       const double post_threshold = pol.threshold(inc_obj);
-      for (int b = 0; b < m; ++b) {  // :243-256
-        if (pr.status[b] == BNBG_PRUNABLE) continue;
-        Node& nd = relax_nodes[b];
-        nd.lb = std::max(nd.lb, pr.bounds[b]);
-        if (nd.lb >= post_threshold) continue;
-        const int j = pr.jbranch[b];
-        if (j < 0)
+      if (m > 0) {
+        // prune test, branch variable and children on the device (:243-256)
+        child_slots.resize(2 * (size_t)m);
+        for (int i = 0; i < 2 * m; ++i) child_slots[i] = slots.take();
+        if (int rc = eng.pool_reserve(slots.high_water())) return set_err(h, rc, eng.err);
+        int surv = 0, bad = -1;
+        const int rc = eng.branch_pool(m, batch_slots.data(), batch_lb.data(), post_threshold,
+                                       child_slots.data(), surv, bad, rec, rec_lb);
+        if (rc) return set_err(h, rc, eng.err);
+        if (bad >= 0)
           return set_err(h, BNBG_LOGIC_ERROR, "select_branch_variable: no free coordinate");
-        Node c0, c1;
-        branch(nd, j, pr.beta.data() + (size_t)b * p, k, M, p, c0, c1, st, st2);
-        for (Node* child : {&c0, &c1}) {
-          if (child->is_leaf(k, p))
-            pending.push_back(std::move(*child));
-          else
-            queue.push(std::move(*child));
+        for (int i = 2 * m - 1; i >= 2 * surv; --i) slots.give(child_slots[i]);
+        const int RI = 4 + kk;
+        for (int c = 0; c < 2 * surv; ++c) {
+          const int* r = rec.data() + (size_t)c * RI;
+          if (r[1]) {  // leaf child -> pending_leaves (node_model.hpp:33-36)
+            pending.push_back(Leaf{rec_lb[c], std::vector<int>(r + 4, r + 4 + r[2])});
+            slots.give(r[0]);
+          } else {
+            queue.push(rec_lb[c], r[0]);
+          }
         }
+        for (int s : batch_slots) slots.give(s);
       }
     }
     if (on_boundary) {  // :259-265
       double lb = queue.global_lb();
-      for (const Node& leaf : pending) lb = std::min(lb, leaf.lb);
+      for (const Leaf& leaf : pending) lb = std::min(lb, leaf.lb);
       on_boundary(user, std::min(lb, inc_obj), inc_obj);
     }
   }
@@ -412,7 +374,7 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
     cert->gap_percent = 0.0;
   } else {
     double lb = queue.global_lb();
-    for (const Node& leaf : pending) lb = std::min(lb, leaf.lb);
+    for (const Leaf& leaf : pending) lb = std::min(lb, leaf.lb);
     lb = std::min(lb, ub);
     cert->lower_bound = lb;
     cert->gap_percent =

@@ -59,10 +59,11 @@ cudaError_t launch_eval(int E, int m, size_t smem, cudaStream_t st, const RelaxD
 
 cudaError_t launch_round_select(int E, int m, size_t smem, cudaStream_t st, int p, int n2, int k,
                                 const double* beta, const uint8_t* state, const int* kbar,
-                                const int* one_off, const int* one_idx, int* sup, int* len,
-                                int* jb) {
+                                const int* one_off, const int* one_idx, const int* one_len, int* sup,
+                                int* len, int* jb) {
   DISPATCH_E(E, k_round_select<EV><<<m, kNodeThreads, smem, st>>>(p, n2, k, beta, state, kbar,
-                                                                  one_off, one_idx, sup, len, jb));
+                                                                  one_off, one_idx, one_len, sup,
+                                                                  len, jb));
   return cudaGetLastError();
 }
 

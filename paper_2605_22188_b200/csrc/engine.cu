@@ -61,6 +61,18 @@ Engine::~Engine() {
   cudaFree(dPassOut_);
   cudaFree(dPassProf_);
   cudaFree(dBar_);
+  for (void* q : pool_mem_) cudaFree(q);
+  cudaFree(dSlots_);
+  cudaFree(dLbIn_);
+  cudaFree(dLbOut_);
+  cudaFree(dPos_);
+  cudaFree(dTot_);
+  cudaFree(dFree_);
+  cudaFree(dRec_);
+  cudaFree(dRecLb_);
+  cudaFree(dOneLen_);
+  cudaFree(dOneIdx_);
+  cudaFree(dLists_);
   if (hPin_) cudaFreeHost(hPin_);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
@@ -584,7 +596,7 @@ int Engine::run_pass(int m, const RelaxParams& cfg, double thr, double eta, doub
 
 int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_trace,
                            PassResult& out, bool round_select, const int* d_one_off,
-                           const int* d_one_idx) {
+                           const int* d_one_idx, const int* d_one_len, bool read_beta) {
   const double eta = 1.0 / L;  // relaxation.hpp:177-180
   const double rho = 1.0 / (2.0 * eta * lambda2);
   const int max_evals = cfg.max_iterations / std::max(1, cfg.check_interval) + 2;
@@ -625,14 +637,14 @@ int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_
   }
   out.iterations = iter;
   out.node_iterations = node_its;
-  out.beta.resize((size_t)p * m);
+  if (read_beta) out.beta.resize((size_t)p * m);
   out.bounds.resize(m);
   out.status.resize(m);
   out.iters.resize(m);
   if (round_select) {
     ++launches;
     CK(launch_round_select(colE_, m, csmem_, stream_, p, n2_, std::max(k, 1), dB_, dState_, dKbar_,
-                           d_one_off, d_one_idx, dSup_, dLen_, dJb_));
+                           d_one_off, d_one_idx, d_one_len, dSup_, dLen_, dJb_));
     out.sup.resize((size_t)m * std::max(k, 1));
     out.len.resize(m);
     out.jbranch.resize(m);
@@ -640,7 +652,11 @@ int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_
     if (int rc_ = d2h(out.len.data(), dLen_, sizeof(int) * m)) return rc_;
     if (int rc_ = d2h(out.jbranch.data(), dJb_, sizeof(int) * m)) return rc_;
   }
-  if (int rc_ = d2h(out.beta.data(), dB_, sizeof(double) * (size_t)p * m)) return rc_;
+  if (read_beta) {
+    if (int rc_ = d2h(out.beta.data(), dB_, sizeof(double) * (size_t)p * m)) return rc_;
+  } else {
+    out.beta.clear();
+  }
   if (int rc_ = d2h(out.bounds.data(), dBest_, sizeof(double) * m)) return rc_;
   if (int rc_ = d2h(out.status.data(), dStatus_, sizeof(int) * m)) return rc_;
   if (int rc_ = d2h(out.iters.data(), dIters_, sizeof(int) * m)) return rc_;
@@ -668,7 +684,7 @@ int Engine::relax_raw(int m, const RelaxParams& cfg, double thr, const uint8_t* 
                                               dFrozen_, dStatus_, dIters_, dAct_,
                                               cfg.max_iterations);
   CKL("k_init_cols");
-  return relax_uploaded(m, cfg, thr, trace, out, false, nullptr, nullptr);
+  return relax_uploaded(m, cfg, thr, trace, out, false, nullptr, nullptr, nullptr, true);
 }
 
 int Engine::relax_lists(const BatchLists& L_, const double* warm, const RelaxParams& cfg,
@@ -696,7 +712,7 @@ int Engine::relax_lists(const BatchLists& L_, const double* warm, const RelaxPar
                                  dWarm, dB_, dV_, dT_, dBest_, dLast_, dFrozen_, dStatus_, dIters_,
                                  dAct_, cfg.max_iterations);
   CKL("k_pack");
-  return relax_uploaded(m, cfg, thr, trace, out, true, do_off, do_idx);
+  return relax_uploaded(m, cfg, thr, trace, out, true, do_off, do_idx, nullptr, true);
 }
 
 int Engine::round_select(int m, const double* beta, const uint8_t* state, const int32_t* kbar,
@@ -718,7 +734,8 @@ int Engine::round_select(int m, const double* beta, const uint8_t* state, const 
   }
   ++launches;
   CK(launch_round_select(colE_, m, csmem_, stream_, p, n2_, std::max(k, 1), dB_, dState_, dKbar_,
-                         one_off ? d_off : nullptr, one_off ? d_idx : nullptr, dSup_, dLen_, dJb_));
+                         one_off ? d_off : nullptr, one_off ? d_idx : nullptr, nullptr, dSup_, dLen_,
+                         dJb_));
   if (sup)
     if (int rc_ = d2h(sup, dSup_, sizeof(int) * (size_t)m * std::max(k, 1))) return rc_;
   if (len) if (int rc_ = d2h(len, dLen_, sizeof(int) * m)) return rc_;

@@ -57,7 +57,7 @@ class Engine {
   // solve_batch_relaxation over columns already uploaded (state/kbar/B)
   int relax_uploaded(int m, const RelaxParams& cfg, double prune_threshold, bool trace,
                      PassResult& out, bool round_select, const int* d_one_off,
-                     const int* d_one_idx);
+                     const int* d_one_idx, const int* d_one_len, bool read_beta);
   // bnbg_relax_batch: raw state/kbar/warm from the host
   int relax_raw(int m, const RelaxParams& cfg, double prune_threshold, const uint8_t* state,
                 const int32_t* kbar, const double* warm, bool trace, PassResult& out);
@@ -70,6 +70,24 @@ class Engine {
                    const int32_t* one_off, const int32_t* one_idx, int32_t* sup, int32_t* len,
                    int32_t* jb);
   int gemm_probe(int trans, int m, const double* B, double* C);
+
+  // ---- device-resident node pool (pool.cu, pool_kernels.cuh) ----
+  int pool_reserve(int cap);  // grow the pool to >= cap slots (contents kept)
+  int pool_root(int slot);    // root_node (node_model.hpp:47-52) in `slot`
+  int pool_capacity() const { return pool_cap_; }
+  // one pass of lower bounds + rounding + branch selection over pool slots;
+  // no warm start or beta crosses PCIe.  With `lists`, the batch's J0/J1
+  // lists are read back (DebugHooks): n01 m x 2, j0 m x p, j1 m x k.
+  int relax_pool(int m, const int* slots, const RelaxParams& cfg, double prune_threshold,
+                 bool trace, PassResult& out, bool lists, std::vector<int>* n01,
+                 std::vector<int>* j0, std::vector<int>* j1);
+  // prune test + branch (bnb_engine.hpp:242-256, node_model.hpp:57-105) of the
+  // last relax_pool batch: children go to free_slots[0 .. 2 survivors); one
+  // record per child (slot, leaf, |J1|, depth, J1 list) plus its lower bound.
+  // bad_column >= 0 reports a survivor without a free coordinate.
+  int branch_pool(int m, const int* slots, const double* lb_in, double post_threshold,
+                  const int* free_slots, int& survivors, int& bad_column, std::vector<int>& rec,
+                  std::vector<double>& rec_lb);
 
   int n = 0, p = 0, k = 0, loss = 0, device = 0;
   double M = 1.0, lambda2 = 1.0, L = 0.0;
@@ -84,6 +102,21 @@ class Engine {
 
  private:
   int ensure(int m);
+  int pool_cap_ = 0;
+  void* pool_mem_[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  int* dSlots_ = nullptr;    // batch slot ids (m)
+  double* dLbIn_ = nullptr;  // parents' lower bounds (m)
+  double* dLbOut_ = nullptr;
+  int* dPos_ = nullptr;      // child position of each survivor (m)
+  int* dTot_ = nullptr;      // [0] survivors, [1] first bad column
+  int* dFree_ = nullptr;     // free slots for children (2m)
+  int* dRec_ = nullptr;      // child records (2m x (4 + k))
+  double* dRecLb_ = nullptr; // (2m)
+  int* dOneLen_ = nullptr;   // padded J1 lists of the batch (m, m x k)
+  int* dOneIdx_ = nullptr;
+  int* dLists_ = nullptr;    // DebugHooks list readback scratch
+  int pool_batch_cap_ = 0;
+  int ensure_pool_batch(int m);
   int ensure_aux(size_t bytes);
   int fail(int code, const std::string& msg);
   int cuda_fail(cudaError_t e, const char* what);

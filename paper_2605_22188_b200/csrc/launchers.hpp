@@ -56,8 +56,8 @@ cudaError_t launch_eval(int E, int m, size_t smem, cudaStream_t st, const RelaxD
                         const EvalArgs& e);
 cudaError_t launch_round_select(int E, int m, size_t smem, cudaStream_t st, int p, int n2, int k,
                                 const double* beta, const uint8_t* state, const int* kbar,
-                                const int* one_off, const int* one_idx, int* sup, int* len,
-                                int* jb);
+                                const int* one_off, const int* one_idx, const int* one_len, int* sup,
+                                int* len, int* jb);
 cudaError_t launch_prox_standalone(int E, int m, size_t smem, cudaStream_t st, int mode, int p,
                                    int n2, const double* U, const uint8_t* state, const int* kbar,
                                    double w, double M, double* out);

@@ -932,7 +932,8 @@ static __global__ void __launch_bounds__(1024) k_compact(int* act, int* d_ma, co
 template <int E>
 __global__ void __launch_bounds__(kNodeThreads)
     k_round_select(int p, int n2, int k, const double* beta, const uint8_t* state, const int* kbar,
-                   const int* one_off, const int* one_idx, int* sup, int* len, int* jbranch) {
+                   const int* one_off, const int* one_idx, const int* one_len, int* sup, int* len,
+                   int* jbranch) {
   extern __shared__ __align__(16) double sm[];
   const int b = blockIdx.x;
   const ColSmem S = col_smem(sm, p, n2, E);
@@ -942,7 +943,9 @@ __global__ void __launch_bounds__(kNodeThreads)
       p, n2, [&](int j) { return st[j] == kFree ? fabs(bb[j]) : -1.0; }, S.key, S.idx, S.xk, S.xi);
   if (threadIdx.x == 0) {
     int l = 0;
-    if (one_off) {
+    if (one_len) {  // padded lists: column b's J1 at one_idx[b*k, b*k + one_len[b])
+      for (int t = 0; t < one_len[b]; ++t) sup[(size_t)b * k + l++] = one_idx[(size_t)b * k + t];
+    } else if (one_off) {  // CSR lists
       for (int t = one_off[b]; t < one_off[b + 1]; ++t) sup[(size_t)b * k + l++] = one_idx[t];
     }
     const int kb = kbar[b];
