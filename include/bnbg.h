@@ -182,6 +182,43 @@ int bnbg_pool_record(const bnbg_pool* pool, int i, int32_t* seq_out, double* coe
                      double* objective_out);
 void bnbg_pool_free(bnbg_pool* pool);
 
+/* ---- node-sharded multi-GPU solve (no reference counterpart:
+ * the reference only describes node-parallel solving) --
+ * X and y are replicated on every rank's handle; open nodes are sharded
+ * across ranks; per pass only the incumbent, the termination state and (when
+ * a rank starves) queue nodes cross between ranks.  One handle per rank
+ * (one process per GPU). */
+
+/* Host-staged transport supplied by the caller (e.g. torch.distributed over
+ * gloo).  Callbacks return 0 on success. */
+typedef struct {
+  void* ctx;
+  int rank, world;
+  /* recv receives `world` blocks of `bytes` bytes in rank order */
+  int (*allgather)(void* ctx, const void* send, int64_t bytes, void* recv);
+  /* send holds one contiguous block per peer in rank order (send_bytes[peer]
+   * bytes each, possibly 0); recv likewise with recv_bytes[peer] */
+  int (*alltoallv)(void* ctx, const void* send, const int64_t* send_bytes, void* recv,
+                   const int64_t* recv_bytes);
+} bnbg_comm_ops;
+
+/* NCCL bootstrap: rank 0 creates the id, the caller broadcasts its 128 bytes
+ * (e.g. torch.distributed), then every rank binds its handle. */
+int bnbg_nccl_unique_id(uint8_t* uid_out /* 128 bytes */);
+int bnbg_nccl_init(bnbg_handle* h, const uint8_t* uid /* 128 bytes */, int rank, int world);
+
+/* The certified solve of bnbg_solve with nodes sharded over ranks.  ops ==
+ * NULL uses the handle's NCCL communicator (bnbg_nccl_init).  Every rank
+ * receives the same certificate; counters are sums over ranks.  Only the
+ * solve policy (bnb_engine.hpp:304-307) is sharded. */
+int bnbg_solve_sharded(bnbg_handle* h, const bnbg_solver_cfg* cfg, const bnbg_comm_ops* ops,
+                       bnbg_certificate* cert);
+
+/* The deterministic load-balancing plan used by bnbg_solve_sharded (exported
+ * for tests): counts[world] queue sizes -> moves[world*world] (donor-major);
+ * returns 1 when nodes move, 0 otherwise. */
+int bnbg_balance_plan(int world, const int64_t* counts, int64_t* moves);
+
 /* ---- diagnostics ---------------------------------------------------------- */
 /* Number of kernel launches issued by this handle so far (bench gpu_launches). */
 long long bnbg_kernel_launches(const bnbg_handle* h);

@@ -48,6 +48,7 @@ __all__ = [
     "InputError", "NumericError", "LogicError", "CudaError", "validate", "generate_synthetic",
     "smoothness_constant", "auto_batch_size", "solve", "collect_rashomon", "prox_step",
     "batched_conjugate_prox", "g_value", "g_conjugate_value", "root_node", "lib_path",
+    "balance_plan", "solve_sharded",
 ]
 
 
@@ -507,6 +508,18 @@ class Engine:
         _check(_L.lib().bnbg_solve(self._h, C.byref(cfg), C.byref(cc), dh, bh, None), self._h)
         return _cert_from_c(cc, sup, coef)
 
+    # -- node-sharded solve over ranks (include/bnbg.h) ------------
+    def solve_sharded(self, config: Optional[SolverConfig] = None, group=None,
+                      transport: Optional[str] = None) -> Certificate:
+        """Certified solve with the open nodes sharded over the ranks of a
+        torch.distributed group (one process and one Engine per GPU, X and y
+        replicated).  transport "nccl": the engine's own NCCL communicator
+        (device-to-device node exchange; the default when the group's backend
+        is NCCL); "host": node records staged through host memory over the
+        group (gloo) -- for CPU-driven tests and several ranks on one GPU."""
+        from . import sharded
+        return sharded.solve_sharded(self, config, group, transport)
+
     # -- rashomon.hpp:149-218 ---------------------------------------------------
     def collect_rashomon(self, config: Optional[SolverConfig] = None,
                          rconfig: Optional[RashomonConfig] = None) -> RashomonResult:
@@ -534,6 +547,16 @@ class Engine:
         return RashomonResult(_cert_from_c(cc, sup, coef), recs)
 
 
+def balance_plan(counts) -> Optional[np.ndarray]:
+    """The sharded solve's deterministic load-balancing plan: queue sizes per
+    rank -> moves[donor, receiver], or None when nothing moves."""
+    c = np.ascontiguousarray(np.asarray(counts, dtype=np.int64))
+    w = len(c)
+    mv = np.zeros(w * w, dtype=np.int64)
+    moved = _L.lib().bnbg_balance_plan(w, c, mv)
+    return mv.reshape(w, w) if moved else None
+
+
 def smoothness_constant(kind: int, X: np.ndarray, device: int = 0) -> float:
     """losses.hpp:86-112 (power iteration on the device)."""
     X = np.asfortranarray(X, dtype=np.float64)
@@ -552,6 +575,19 @@ def solve(inst: ProblemInstance, config: Optional[SolverConfig] = None,
     cfg = config or SolverConfig()
     with Engine(inst, device, cfg.relax.smoothness) as eng:
         return eng.solve(cfg, hooks)
+
+
+def solve_sharded(inst: ProblemInstance, config: Optional[SolverConfig] = None, group=None,
+                  transport: Optional[str] = None, device: Optional[int] = None) -> Certificate:
+    """Node-sharded certified solve: one process per GPU in a torch.distributed
+    group, X and y replicated, open nodes dealt over the ranks (include/bnbg.h
+    bnbg_solve_sharded).  device defaults to the current CUDA device."""
+    cfg = config or SolverConfig()
+    if device is None:
+        import torch
+        device = torch.cuda.current_device()
+    with Engine(inst, device, cfg.relax.smoothness) as eng:
+        return eng.solve_sharded(cfg, group, transport)
 
 
 def collect_rashomon(inst: ProblemInstance, config: Optional[SolverConfig] = None,

@@ -41,6 +41,16 @@ class CertC(C.Structure):
                 ("reopt_supports", C.c_longlong), ("device_seconds", C.c_double)]
 
 
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+ALLTOALLV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p,
+                           C.POINTER(C.c_int64))
+
+
+class CommOpsC(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("rank", C.c_int), ("world", C.c_int),
+                ("allgather", ALLGATHER_FN), ("alltoallv", ALLTOALLV_FN)]
+
+
 TRACE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.c_double)
 DUAL_HOOK = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.POINTER(C.c_int32), C.c_int,
                         C.POINTER(C.c_int32), C.c_double)
@@ -59,7 +69,8 @@ EXPORTS = [
     "bnbg_g_value", "bnbg_g_conjugate", "bnbg_gemm", "bnbg_solve", "bnbg_collect_rashomon",
     "bnbg_pool_size", "bnbg_pool_record", "bnbg_pool_free", "bnbg_kernel_launches",
     "bnbg_gemm_stats", "bnbg_set_timing", "bnbg_kernel_stats", "bnbg_transfer_bytes",
-    "bnbg_pass_profile",
+    "bnbg_pass_profile", "bnbg_nccl_unique_id", "bnbg_nccl_init", "bnbg_solve_sharded",
+    "bnbg_balance_plan",
 ]
 
 
@@ -113,5 +124,11 @@ def lib():
     L.bnbg_kernel_stats.argtypes = [vp, i, C.POINTER(d), C.POINTER(d), C.POINTER(ll)]
     L.bnbg_transfer_bytes.argtypes = [vp, C.POINTER(ll), C.POINTER(ll)]
     L.bnbg_pass_profile.argtypes = [vp, dp, i]
+    L.bnbg_nccl_unique_id.argtypes = [C.c_char_p]
+    L.bnbg_nccl_init.argtypes = [vp, C.c_char_p, i, i]
+    L.bnbg_solve_sharded.argtypes = [vp, C.POINTER(SolverCfgC), C.POINTER(CommOpsC),
+                                     C.POINTER(CertC)]
+    i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+    L.bnbg_balance_plan.argtypes = [i, i64p, i64p]
     _lib = L
     return L

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "../../include/bnbg.h"
+#include "comm.hpp"
 #include "engine.hpp"
 #include "rng.hpp"
 
@@ -67,6 +68,7 @@ class NodeQueue {
  public:
   void push(double lb, int slot) { heap_.push(QEntry{lb, seq_++, slot}); }
   bool empty() const { return heap_.empty(); }
+  size_t size() const { return heap_.size(); }
   double global_lb() const { return heap_.empty() ? kInf : heap_.top().bound; }
   QEntry pop() {
     QEntry e = heap_.top();
@@ -184,9 +186,19 @@ bnbg::RelaxParams relax_params(const bnbg_relax_cfg& c) {
   return r;
 }
 
-// bnb_engine.hpp:116-291 run_bnb
+// Incumbent record exchanged between ranks: objective, |support|, support
+// (sorted) and coefficients, as doubles.
+struct IncRecord {
+  static size_t doubles(int k) { return 2 + 2 * (size_t)k; }
+};
+
+// bnb_engine.hpp:116-291 run_bnb.  With `comm` the nodes are sharded over
+// ranks (comm.hpp): rank 0 starts with the root, every pass ends with the
+// incumbent exchange, the termination/time-limit exchange and, when a rank
+// starves, a node exchange between the ranks' device pools.
 int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certificate* cert,
-            bnbg_dual_hook on_dual, bnbg_boundary_hook on_boundary, void* user) {
+            bnbg_dual_hook on_dual, bnbg_boundary_hook on_boundary, void* user,
+            bnbg::Comm* comm = nullptr) {
   bnbg::Engine& eng = h->eng;
   const int n = eng.n, p = eng.p, k = eng.k;
   const double M = eng.M;
@@ -216,11 +228,14 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
 
   NodeQueue queue;
   SlotAllocator slots;
-  {
+  const int rank = comm ? comm->rank : 0, world = comm ? comm->world : 1;
+  if (rank == 0) {
     const int root = slots.take();  // root_node (node_model.hpp:47-52)
     if (int rc = eng.pool_root(root)) return set_err(h, rc, eng.err);
     queue.push(-kInf, root);
   }
+  int64_t global_open = 1;  // sharded: open nodes over all ranks after the last pass
+  bool global_stop = false;
   std::vector<Leaf> pending;
   double inc_obj = kInf;
   std::vector<int> inc_sup;
@@ -231,8 +246,8 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
   std::vector<double> batch_lb, rec_lb;
   const int kk = std::max(k, 1);
 
-  while (!queue.empty() || !pending.empty()) {
-    if (elapsed() > cfg.time_limit) {
+  while (comm ? global_open > 0 : (!queue.empty() || !pending.empty())) {
+    if (comm ? global_stop : elapsed() > cfg.time_limit) {
       status = BNBG_STATUS_TIME_LIMIT;
       break;
     }
@@ -263,7 +278,7 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
       pending.clear();
     }
     const int m = (int)batch_slots.size();
-    if (m == 0 && leaves.empty()) continue;
+    if (!comm && m == 0 && leaves.empty()) continue;
 
     if (m > 0) {
       Timer t(cert->lower_bound_seconds);
@@ -328,6 +343,32 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
           }
         }
       }
+      if (comm) {  // global incumbent: lowest objective, ties to the lowest rank
+        const size_t R = IncRecord::doubles(kk);
+        std::vector<double> mine(R, 0.0), all(R * world);
+        mine[0] = inc_obj;
+        mine[1] = (double)inc_sup.size();
+        for (size_t i = 0; i < inc_sup.size(); ++i) {
+          mine[2 + i] = (double)inc_sup[i];
+          mine[2 + kk + i] = inc_coef[i];
+        }
+        if (int rc = comm->allgather(eng, mine.data(), sizeof(double) * R, all.data()))
+          return set_err(h, rc, eng.err);
+        int win = -1;
+        for (int r = 0; r < world; ++r)
+          if (win < 0 || all[R * r] < all[R * win]) win = r;
+        const double* w = all.data() + R * win;
+        if (w[0] < inc_obj || (w[0] == inc_obj && win < rank)) {
+          inc_obj = w[0];
+          const int len = (int)w[1];
+          inc_sup.resize(len);
+          inc_coef.resize(len);
+          for (int i = 0; i < len; ++i) {
+            inc_sup[i] = (int)w[2 + i];
+            inc_coef[i] = w[2 + kk + i];
+          }
+        }
+      }
       const double post_threshold = pol.threshold(inc_obj);
       if (m > 0) {
         // prune test, branch variable and children on the device (:243-256)
@@ -354,6 +395,71 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
         for (int s : batch_slots) slots.give(s);
       }
     }
+    if (comm) {  // termination, time limit and load balance over the ranks
+      Timer t(cert->transfer_seconds);
+      double lb_local = queue.global_lb();
+      for (const Leaf& leaf : pending) lb_local = std::min(lb_local, leaf.lb);
+      const double mine[4] = {(double)queue.size(), (double)pending.size(), lb_local,
+                              elapsed() > cfg.time_limit ? 1.0 : 0.0};
+      std::vector<double> all(4 * (size_t)world);
+      if (int rc = comm->allgather(eng, mine, sizeof(mine), all.data()))
+        return set_err(h, rc, eng.err);
+      global_open = 0;
+      global_stop = false;
+      std::vector<int64_t> counts(world), moves((size_t)world * world);
+      for (int r = 0; r < world; ++r) {
+        counts[r] = (int64_t)all[4 * r];
+        global_open += counts[r] + (int64_t)all[4 * r + 1];
+        global_stop = global_stop || all[4 * r + 3] != 0.0;
+      }
+      if (global_open > 0 && !global_stop &&
+          bnbg::balance_plan(world, counts.data(), moves.data())) {
+        // donors hand over every other node from the top of their queue
+        std::vector<int64_t> send_n(world, 0), recv_n(world, 0);
+        int64_t nsend = 0, nrecv = 0;
+        for (int r = 0; r < world; ++r) {
+          send_n[r] = moves[(size_t)rank * world + r];
+          recv_n[r] = moves[(size_t)r * world + rank];
+          nsend += send_n[r];
+          nrecv += recv_n[r];
+        }
+        std::vector<int> send_slots;
+        std::vector<double> send_lb;
+        if (nsend > 0) {
+          std::vector<QEntry> keep;
+          int idx = 0;
+          while ((int64_t)send_slots.size() < nsend && !queue.empty()) {
+            const QEntry e = queue.pop();
+            const int64_t need = nsend - (int64_t)send_slots.size();
+            if (idx % 2 == 1 || (int64_t)queue.size() < need) {
+              send_slots.push_back(e.slot);
+              send_lb.push_back(e.bound);
+            } else {
+              keep.push_back(e);
+            }
+            ++idx;
+          }
+          for (const QEntry& e : keep) queue.push(e.bound, e.slot);
+        }
+        uint8_t* d_send = nullptr;
+        uint8_t* d_recv = nullptr;
+        if (int rc = eng.pool_pack((int)nsend, send_slots.data(), send_lb.data(), &d_send))
+          return set_err(h, rc, eng.err);
+        if (int rc = eng.pool_recv_buffer((int)nrecv, &d_recv)) return set_err(h, rc, eng.err);
+        if (int rc = comm->exchange(eng, send_n, d_send, recv_n, d_recv, eng.node_record_bytes()))
+          return set_err(h, rc, eng.err);
+        for (int s : send_slots) slots.give(s);
+        if (nrecv > 0) {
+          std::vector<int> rslots(nrecv);
+          for (auto& s : rslots) s = slots.take();
+          if (int rc = eng.pool_reserve(slots.high_water())) return set_err(h, rc, eng.err);
+          std::vector<double> rlb(nrecv);
+          if (int rc = eng.pool_unpack((int)nrecv, rslots.data(), rlb.data()))
+            return set_err(h, rc, eng.err);
+          for (int64_t i = 0; i < nrecv; ++i) queue.push(rlb[i], rslots[i]);
+        }
+      }
+    }
     if (on_boundary) {  // :259-265
       double lb = queue.global_lb();
       for (const Leaf& leaf : pending) lb = std::min(lb, leaf.lb);
@@ -361,6 +467,29 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
     }
   }
 
+  double lb_open = queue.global_lb();
+  for (const Leaf& leaf : pending) lb_open = std::min(lb_open, leaf.lb);
+  if (comm) {  // counters are sums over ranks; the open bound is the global minimum
+    const double mine[7] = {(double)cert->nodes_processed, (double)cert->lb_batches,
+                            (double)cert->reopt_batches,   (double)cert->relax_iterations,
+                            (double)cert->node_iterations, (double)cert->reopt_supports,
+                            lb_open};
+    std::vector<double> all(7 * (size_t)world);
+    if (int rc = comm->allgather(eng, mine, sizeof(mine), all.data()))
+      return set_err(h, rc, eng.err);
+    double tot[6] = {0, 0, 0, 0, 0, 0};
+    lb_open = kInf;
+    for (int r = 0; r < world; ++r) {
+      for (int q = 0; q < 6; ++q) tot[q] += all[7 * r + q];
+      lb_open = std::min(lb_open, all[7 * r + 6]);
+    }
+    cert->nodes_processed = (long long)tot[0];
+    cert->lb_batches = (long long)tot[1];
+    cert->reopt_batches = (long long)tot[2];
+    cert->relax_iterations = (long long)tot[3];
+    cert->node_iterations = (long long)tot[4];
+    cert->reopt_supports = (long long)tot[5];
+  }
   const double ub = inc_obj;  // certificate (:268-290)
   cert->status = status;
   cert->optimal_value = ub;
@@ -373,9 +502,7 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
     cert->lower_bound = ub;
     cert->gap_percent = 0.0;
   } else {
-    double lb = queue.global_lb();
-    for (const Leaf& leaf : pending) lb = std::min(lb, leaf.lb);
-    lb = std::min(lb, ub);
+    const double lb = std::min(lb_open, ub);
     cert->lower_bound = lb;
     cert->gap_percent =
         !std::isfinite(ub) ? 100.0 : 100.0 * (ub - lb) / std::max(std::fabs(ub), 1e-12);
@@ -594,6 +721,44 @@ int bnbg_solve(bnbg_handle* h, const bnbg_solver_cfg* cfg, bnbg_certificate* cer
   pol.delta = c.prune_slack;
   const double saved_L = h->eng.L;
   const int rc = run_bnb(h, c, pol, cert, on_dual, on_boundary, user);
+  h->eng.L = saved_L;
+  return rc;
+}
+
+int bnbg_nccl_init(bnbg_handle* h, const uint8_t* uid, int rank, int world) {
+  if (world < 1 || rank < 0 || rank >= world)
+    return set_err(h, BNBG_INPUT_ERROR, "nccl_init: rank must lie in [0, world)");
+  const int rc = h->eng.nccl_init(uid, rank, world);
+  return rc ? set_err(h, rc, h->eng.err) : BNBG_OK;
+}
+
+int bnbg_solve_sharded(bnbg_handle* h, const bnbg_solver_cfg* cfg, const bnbg_comm_ops* ops,
+                       bnbg_certificate* cert) {
+  bnbg_solver_cfg c;
+  if (cfg)
+    c = *cfg;
+  else
+    bnbg_solver_cfg_default(&c);
+  Policy pol;
+  pol.kind = 0;
+  pol.delta = c.prune_slack;
+  std::unique_ptr<bnbg::Comm> comm;
+  if (ops) {
+    if (ops->world < 1 || ops->rank < 0 || ops->rank >= ops->world || !ops->allgather ||
+        !ops->alltoallv)
+      return set_err(h, BNBG_INPUT_ERROR, "solve_sharded: invalid communicator");
+    comm.reset(new bnbg::CallbackComm(ops));
+  } else {
+    if (!h->eng.nccl_comm)
+      return set_err(h, BNBG_INPUT_ERROR, "solve_sharded: no communicator (bnbg_nccl_init)");
+    auto* nc = new bnbg::NcclComm();
+    nc->comm = h->eng.nccl_comm;
+    nc->rank = h->eng.nccl_rank;
+    nc->world = h->eng.nccl_world;
+    comm.reset(nc);
+  }
+  const double saved_L = h->eng.L;
+  const int rc = run_bnb(h, c, pol, cert, nullptr, nullptr, nullptr, comm.get());
   h->eng.L = saved_L;
   return rc;
 }

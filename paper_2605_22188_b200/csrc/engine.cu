@@ -61,6 +61,7 @@ Engine::~Engine() {
   cudaFree(dPassOut_);
   cudaFree(dPassProf_);
   cudaFree(dBar_);
+  comm_release();
   for (void* q : pool_mem_) cudaFree(q);
   cudaFree(dSlots_);
   cudaFree(dLbIn_);

@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "../../include/bnbg.h"
 #include "launchers.hpp"
 
 namespace bnbg {
@@ -89,6 +90,25 @@ class Engine {
                   const int* free_slots, int& survivors, int& bad_column, std::vector<int>& rec,
                   std::vector<double>& rec_lb);
 
+  // ---- multi-GPU node exchange (comm.cu) ----
+  size_t node_record_bytes() const;
+  // pack `cnt` pool slots (with their bounds) into the send staging buffer
+  int pool_pack(int cnt, const int* slots, const double* lbs, uint8_t** d_send);
+  // receive staging buffer of `cnt` records
+  int pool_recv_buffer(int cnt, uint8_t** d_recv);
+  // unpack `cnt` received records into pool `slots`; bounds to lbs (host)
+  int pool_unpack(int cnt, const int* slots, double* lbs);
+  int comm_allgather_nccl(const void* send, size_t bytes, void* recv);
+  int comm_exchange_nccl(int world, const int64_t* send_nodes, const uint8_t* d_send,
+                         const int64_t* recv_nodes, uint8_t* d_recv, size_t rec_bytes);
+  int comm_exchange_host(const bnbg_comm_ops* ops, const int64_t* send_nodes,
+                         const uint8_t* d_send, const int64_t* recv_nodes, uint8_t* d_recv,
+                         size_t rec_bytes);
+  int nccl_init(const uint8_t* uid, int rank, int world);
+  void comm_release();
+  void* nccl_comm = nullptr;  // ncclComm_t
+  int nccl_rank = 0, nccl_world = 1;
+
   int n = 0, p = 0, k = 0, loss = 0, device = 0;
   double M = 1.0, lambda2 = 1.0, L = 0.0;
   long long launches = 0;
@@ -117,6 +137,14 @@ class Engine {
   int* dLists_ = nullptr;    // DebugHooks list readback scratch
   int pool_batch_cap_ = 0;
   int ensure_pool_batch(int m);
+  uint8_t* dXSend_ = nullptr;  // node-exchange staging
+  uint8_t* dXRecv_ = nullptr;
+  size_t xsend_bytes_ = 0, xrecv_bytes_ = 0;
+  int* dXSlots_ = nullptr;
+  double* dXLb_ = nullptr;
+  int xslots_cap_ = 0;
+  void* dGather_ = nullptr;  // NCCL allgather scratch
+  size_t gather_bytes_ = 0;
   int ensure_aux(size_t bytes);
   int fail(int code, const std::string& msg);
   int cuda_fail(cudaError_t e, const char* what);

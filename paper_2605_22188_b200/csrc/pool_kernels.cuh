@@ -278,4 +278,70 @@ static __global__ void __launch_bounds__(kPoolThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// node exchange between ranks (multi-GPU load balancing):
+// a node travels as one fixed-size record
+//   [lb f64][n0 i32 n1 i32 depth i32 pad][state p B, padded to 8][warm p f64]
+//   [J0 p i32][J1 k i32, padded to 8]
+// ---------------------------------------------------------------------------
+__host__ __device__ inline size_t node_rec_bytes(int p, int k) {
+  const size_t pad8 = ((size_t)p + 7) & ~(size_t)7;
+  const size_t j1 = ((size_t)4 * k + 7) & ~(size_t)7;
+  return 24 + pad8 + 8 * (size_t)p + 4 * (size_t)p + j1;
+}
+
+static __global__ void k_pool_pack(PoolDev P, int cnt, const int* slots, const double* lbs,
+                                   uint8_t* out) {
+  const int i = blockIdx.x;
+  if (i >= cnt) return;
+  const int s = slots[i], p = P.p, k = P.k;
+  uint8_t* r = out + (size_t)i * node_rec_bytes(p, k);
+  const size_t pad8 = ((size_t)p + 7) & ~(size_t)7;
+  uint8_t* st = r + 24;
+  double* w = reinterpret_cast<double*>(st + pad8);
+  int* j0 = reinterpret_cast<int*>(w + p);
+  int* j1 = j0 + p;
+  const int n0 = P.n0[s], n1 = P.n1[s];
+  for (int j = threadIdx.x; j < p; j += blockDim.x) {
+    st[j] = P.state[(size_t)s * p + j];
+    w[j] = P.warm[(size_t)s * p + j];
+  }
+  for (int q = threadIdx.x; q < n0; q += blockDim.x) j0[q] = P.j0[(size_t)s * p + q];
+  for (int q = threadIdx.x; q < n1; q += blockDim.x) j1[q] = P.j1[(size_t)s * k + q];
+  if (threadIdx.x == 0) {
+    *reinterpret_cast<double*>(r) = lbs[i];
+    int* hd = reinterpret_cast<int*>(r + 8);
+    hd[0] = n0;
+    hd[1] = n1;
+    hd[2] = P.depth[s];
+  }
+}
+
+static __global__ void k_pool_unpack(PoolDev P, int cnt, const uint8_t* in, const int* slots,
+                                     double* lbs) {
+  const int i = blockIdx.x;
+  if (i >= cnt) return;
+  const int s = slots[i], p = P.p, k = P.k;
+  const uint8_t* r = in + (size_t)i * node_rec_bytes(p, k);
+  const size_t pad8 = ((size_t)p + 7) & ~(size_t)7;
+  const uint8_t* st = r + 24;
+  const double* w = reinterpret_cast<const double*>(st + pad8);
+  const int* j0 = reinterpret_cast<const int*>(w + p);
+  const int* j1 = j0 + p;
+  const int* hd = reinterpret_cast<const int*>(r + 8);
+  const int n0 = hd[0], n1 = hd[1];
+  for (int j = threadIdx.x; j < p; j += blockDim.x) {
+    P.state[(size_t)s * p + j] = st[j];
+    P.warm[(size_t)s * p + j] = w[j];
+  }
+  for (int q = threadIdx.x; q < n0; q += blockDim.x) P.j0[(size_t)s * p + q] = j0[q];
+  for (int q = threadIdx.x; q < n1; q += blockDim.x) P.j1[(size_t)s * k + q] = j1[q];
+  if (threadIdx.x == 0) {
+    P.n0[s] = n0;
+    P.n1[s] = n1;
+    P.depth[s] = hd[2];
+    lbs[i] = *reinterpret_cast<const double*>(r);
+  }
+}
+
 }  // namespace bnbg
