@@ -7,6 +7,11 @@ regression n=2000, p=500, k=8, rho=0.7, seed 0, M=2, lambda2=1; the other
 configs are parity-test cases).  value = nodes processed / second over the
 timed steps (whole job: all ranks); ms_per_step = time-to-certify.
 
+With N > 1 ranks (torchrun) the same instance is certified by the
+node-sharded solve (bnbg_solve_sharded over NCCL: X replicated, open nodes
+dealt over the GPUs, incumbent / termination / node exchange per pass), so
+the total work is fixed ("scaling": "strong").
+
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
 --impl reference times the reference algorithm's CPU implementation (the C
@@ -32,6 +37,10 @@ CONFIGS = {
     "c1": (1000, 100, 5, 0.5, 0, "synthetic sparse linear regression n=1000 p=100 k=5 rho=0.5"),
     "c2": (2000, 500, 8, 0.7, 1, "synthetic sparse logistic regression n=2000 p=500 k=8 rho=0.7"),
     "c3": (5000, 2000, 10, 0.9, 0, "synthetic sparse linear regression n=5000 p=2000 k=10 rho=0.9"),
+    "c4": (20000, 5000, 15, 0.9, 1,
+           "synthetic sparse logistic regression n=20000 p=5000 k=15 rho=0.9 (rho per PAPER.md:1199)"),
+    "c5": (2000, 500, 8, 0.7, 0, "Rashomon set (epsilon 0.01, all supports within 1% of the optimum)"
+                                 " for n=2000 p=500 k=8 rho=0.7 linear regression"),
 }
 METRIC = "BnB nodes/sec at time-to-certify (0 gap)"
 FP64_PEAK_TFLOPS = 37.0  # measured DMMA.8x8x4 issue rate on this pool (profiles/r01_fp64_peak.txt)
@@ -191,6 +200,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=120.0)
+    ap.add_argument("--time-limit", type=float, default=float("inf"),
+                    help="per-certify time limit (c3/c4: nodes/s at a stated limit)")
     args = ap.parse_args()
     spec = CONFIGS[args.config]
     world = _env_int("WORLD_SIZE", 1)
@@ -213,12 +224,17 @@ def main():
     n, p, k, rho, loss, desc = spec
     inst, _ = P.generate_synthetic(P.GeneratorSpec(n=n, p=p, k=k, correlation=rho, loss=loss,
                                                    seed=0, M=2.0, lambda2=1.0))
-    cfg = P.SolverConfig()
+    cfg = P.SolverConfig(time_limit=args.time_limit)
     eng = P.Engine(inst, device=local)  # X, y resident in HBM before timing
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > L2
 
+    def certify(engine):
+        if args.config == "c5":  # collect_rashomon (rashomon.hpp:149-218): same hot path
+            return engine.collect_rashomon(cfg, P.RashomonConfig(epsilon=0.01)).certificate
+        return engine.solve_sharded(cfg, transport="nccl") if world > 1 else engine.solve(cfg)
+
     for _ in range(args.warmup):
-        eng.solve(cfg)
+        certify(eng)
 
     def barrier():
         torch.cuda.synchronize()
@@ -237,7 +253,7 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        cert = eng.solve(cfg)
+        cert = certify(eng)
         e1.record()
         torch.cuda.synchronize()
         total_ms += e0.elapsed_time(e1)
@@ -247,21 +263,17 @@ def main():
     clocks = sampler.stop()
     launches = eng.kernel_launches() - launches0
 
-    t = torch.tensor([total_ms, float(nodes)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if dist:
-        tmax = t.clone()
-        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        tsum = t.clone()
-        dist.all_reduce(tsum[1:], op=dist.ReduceOp.SUM)
-        total_ms_max, nodes_all = float(tmax[0]), float(tsum[1])
-    else:
-        total_ms_max, nodes_all = total_ms, float(nodes)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    # the sharded certificate already reports the nodes of all ranks
+    total_ms_max, nodes_all = float(t[0]), float(nodes)
     value = nodes_all / (total_ms_max / 1e3)
 
     # roofline: one extra (untimed) certify with per-launch CUDA events on the engine stream
     eng.set_timing(True)
     before = eng.kernel_stats()
-    prof_cert = eng.solve(cfg)
+    prof_cert = certify(eng)
     after = eng.kernel_stats()
     eng.set_timing(False)
     delta = {kc: tuple(a - b for a, b in zip(after[kc], before[kc])) for kc in after}
@@ -303,7 +315,7 @@ def main():
         t0 = time.perf_counter()
         e2 = P.Engine(inst, device=local)
         t1 = time.perf_counter()
-        c2 = e2.solve(cfg)
+        c2 = certify(e2)
         bi, bo = e2.transfer_bytes()
         t2 = time.perf_counter()
         e2.close()
@@ -320,7 +332,7 @@ def main():
         te = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_ms = float(te[0])
-    e2e_value = e2e_nodes * world / (e2e_ms / 1e3)
+    e2e_value = e2e_nodes / (e2e_ms / 1e3)
 
     base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -333,11 +345,16 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (generate_synthetic, seed 0, problem.hpp:70-132)",
-            "config": {"workload": f"{args.config}: {desc}, certify to 0 gap",
+            "config": {"workload": f"{args.config}: {desc}, " + (
+                           "certify to 0 gap" if math.isinf(args.time_limit)
+                           else f"nodes/s within a {args.time_limit:g} s time limit"),
                        "n": n, "p": p, "k": k, "rho": rho, "loss": "logistic" if loss else "squared",
-                       "batch_size": c0.batch_size_used, "parallelism": f"replicas{world}",
+                       "batch_size": c0.batch_size_used,
+                       "parallelism": f"node-sharded over {world} GPUs (NCCL)" if world > 1
+                       else "single GPU",
                        "l2": "flushed (256 MiB write) before every step",
                        "time_to_certify_s": total_ms_max / args.steps / 1e3,
                        "nodes_per_certify": c0.nodes_processed, "lb_batches": c0.lb_batches,
