@@ -280,6 +280,20 @@ int Engine::d2h(void* dst, const void* src, size_t bytes) {
 // ---------------------------------------------------------------------------
 Engine::GemmPlan Engine::plan(int Mr, int K, int ncols, bool allow_split) const {
   GemmPlan pl;
+  // wide batches: register-tiled 128 x 64 tiles, no split-K (BNBG_BIGGEMM=0 disables)
+  static const bool big_ok = [] {
+    const char* e = getenv("BNBG_BIGGEMM");
+    return !(e && e[0] == '0');
+  }();
+  if (big_ok && ncols >= 64 && (n % 2) == 0 && (p % 2) == 0) {
+    const int bm = gemm_big_tile_m(), bn = gemm_big_tile_n();
+    pl.big = true;
+    pl.fm = pl.fn = 0;
+    pl.nsplit = 1;
+    pl.ksplit = K;
+    pl.grid = dim3((Mr + bm - 1) / bm, (ncols + bn - 1) / bn, 1);
+    return pl;
+  }
   pl.fn = ncols <= 8 ? 1 : (ncols <= 16 ? 2 : 4);
   const int nt = (ncols + 8 * pl.fn - 1) / (8 * pl.fn);
   pl.fm = 2;
@@ -328,7 +342,10 @@ int Engine::launch_gemm(bool tn, int epi, const GemmPlan& pl, const double* Bsrc
   g.part_conj = dPC_;
   g.part_ld = part_ld;
   ++launches;
-  CK(gemm_launch(tn, epi, pl.fm, pl.fn, pl.grid, stream_, g));
+  if (pl.big)
+    CK(gemm_big_launch(tn, epi, pl.grid, stream_, g));
+  else
+    CK(gemm_launch(tn, epi, pl.fm, pl.fn, pl.grid, stream_, g));
   return 0;
 }
 

@@ -164,6 +164,7 @@ class Engine {
                double* trace, int eval_idx);
   struct GemmPlan {
     int fm, fn, nsplit, ksplit;
+    bool big = false;  // gemm_big.cuh tile (wide batches)
     dim3 grid;
   };
   GemmPlan plan(int M, int K, int ncols, bool allow_split) const;

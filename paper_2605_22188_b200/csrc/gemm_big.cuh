@@ -1,0 +1,180 @@
+// gemm_big.cuh -- register-tiled DMMA GEMM for wide batches (c3/c4 widths).
+//
+// Same contractions and epilogues as gemm.cuh (S = X V[:,act] with l', eval
+// sums; G = X' R[:,act]), for m_a >= 64 active columns where the split-K
+// kernel's cross-warp reductions cost more than they hide:
+//   CTA tile 128 x 64, 8 warps in a 4 (M) x 2 (N) grid, warp tile 32 x 32
+//   (4 x 4 DMMA.8x8x4 fragments, 16 independent accumulators per lane),
+//   BK = 16 (four k-steps) staged through a 3-deep 16-byte cp.async ring
+//   (90 KB: two CTAs, 16 warps per SM).
+// Every output element is accumulated by one lane in k order, so results are
+// deterministic.  Shared-memory strides are = 4 (mod 16) doubles, which makes
+// the fragment loads conflict-free.  Needs n and p even (16-byte rows).
+#pragma once
+#include "gemm.cuh"
+
+namespace bnbg {
+
+constexpr int kBigThreads = 256;
+constexpr int kBigBM = 128, kBigBN = 64, kBigBK = 16, kBigNS = 3;
+constexpr int kBigLDA_NN = kBigBM + 4;  // NN A tile stored [k][m]
+constexpr int kBigLDK = kBigBK + 4;     // [m][k] / [n][k] tiles
+constexpr int kBigA = kBigBK * kBigLDA_NN > kBigBM * kBigLDK ? kBigBK * kBigLDA_NN : kBigBM * kBigLDK;
+constexpr int kBigB = kBigBN * kBigLDK;
+constexpr int kBigStage = kBigA + kBigB;
+constexpr size_t kBigSmemBytes = sizeof(double) * (size_t)kBigNS * kBigStage;
+
+template <bool TN, int EPI>
+__global__ void __launch_bounds__(kBigThreads, 2) k_gemm_big(GemmArgs g) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int colmap[kBigBN];
+  __shared__ double epi_red[2][4][kBigBN];  // EVAL: per-warp-row column sums (l, l*)
+  const int ncols = *g.d_ncols;
+  const int n0 = blockIdx.y * kBigBN;
+  if (n0 >= ncols) return;
+  const int m0 = blockIdx.x * kBigBM;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2;
+  if (tid < kBigBN) {
+    const int c = n0 + tid;
+    colmap[tid] = c < ncols ? (g.act ? g.act[c] : c) : -1;
+  }
+  __syncthreads();
+  const int K = g.K;
+  const int nkt = (K + kBigBK - 1) / kBigBK;
+
+  auto load_stage = [&](int stage, int kt) {
+    double* As = smem + stage * kBigStage;
+    double* Bs = As + kBigA;
+    const int k0 = kt * kBigBK;
+    // A: 128 x 16 doubles = 1024 16-byte chunks
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int e = tid + it * kBigThreads;
+      if (TN) {  // A(m, k) = X[(m0+m)*n + k0 + k], contiguous in k; stored [m][k]
+        const int m = e >> 3, kc = (e & 7) * 2;
+        const int gm = m0 + m, gk = k0 + kc;
+        const bool ok = gm < g.M && gk < K;
+        cp_async_16(As + m * kBigLDK + kc, ok ? g.A + (size_t)gm * g.lda + gk : g.A, ok ? 16 : 0);
+      } else {   // A(m, k) = X[(k0+k)*n + m0 + m], contiguous in m; stored [k][m]
+        const int k = e >> 6, mc = (e & 63) * 2;
+        const int gm = m0 + mc, gk = k0 + k;
+        const bool ok = gm < g.M && gk < K;
+        cp_async_16(As + k * kBigLDA_NN + mc, ok ? g.A + (size_t)gk * g.lda + gm : g.A, ok ? 16 : 0);
+      }
+    }
+    // B: 64 columns x 16 k = 512 chunks
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      const int e = tid + it * kBigThreads;
+      const int c = e >> 3, kc = (e & 7) * 2;
+      const int col = colmap[c];
+      const int gk = k0 + kc;
+      const bool ok = col >= 0 && gk < K;
+      cp_async_16(Bs + c * kBigLDK + kc, ok ? g.B + (size_t)col * g.ldb + gk : g.B, ok ? 16 : 0);
+    }
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < kBigNS - 1; ++s) {
+    if (s < nkt) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nkt; ++kt) {
+    cp_async_wait<kBigNS - 2>();
+    __syncthreads();
+    if (kt + kBigNS - 1 < nkt) load_stage((kt + kBigNS - 1) % kBigNS, kt + kBigNS - 1);
+    cp_async_commit();
+    const double* As = smem + (kt % kBigNS) * kBigStage;
+    const double* Bs = As + kBigA;
+#pragma unroll
+    for (int ks = 0; ks < kBigBK / 4; ++ks) {
+      const int kk = ks * 4 + (lane & 3);
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int row = wm * 32 + i * 8 + (lane >> 2);
+        a[i] = TN ? As[row * kBigLDK + kk] : As[kk * kBigLDA_NN + row];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[(wn * 32 + j * 8 + (lane >> 2)) * kBigLDK + kk];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue: lane holds D[row][col] for row = wm*32 + i*8 + lane/4 and
+  // col = wn*32 + j*8 + 2*(lane%4) + h
+  double lsum[4][2], csum[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) lsum[j][0] = lsum[j][1] = csum[j][0] = csum[j][1] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + wm * 32 + i * 8 + (lane >> 2);
+    const double yv = (EPI != EPI_STORE && gm < g.M) ? g.y[gm] : 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = wn * 32 + j * 8 + (lane & 3) * 2 + h;
+        const int col = colmap[c];
+        if (gm >= g.M || col < 0) continue;
+        const double s = acc[i][j][h];
+        if (EPI == EPI_STORE) {
+          g.C[(size_t)col * g.ldc + gm] = s;
+        } else {
+          const double rv = d_loss_deriv(g.loss, s, yv);
+          g.C[(size_t)col * g.ldc + gm] = rv;
+          if (EPI == EPI_EVAL) {
+            lsum[j][h] += d_loss_value(g.loss, s, yv);
+            csum[j][h] += d_loss_conj(g.loss, rv, yv);
+          }
+        }
+      }
+  }
+  if (EPI == EPI_EVAL) {
+    // column sums over the CTA's 128 rows: lanes sharing lane%4 (8 rows each),
+    // then the 4 warp rows in order
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          lsum[j][h] += __shfl_xor_sync(0xffffffffu, lsum[j][h], o);
+          csum[j][h] += __shfl_xor_sync(0xffffffffu, csum[j][h], o);
+        }
+    if (lane < 4) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = wn * 32 + j * 8 + lane * 2 + h;
+          epi_red[0][wm][c] = lsum[j][h];
+          epi_red[1][wm][c] = csum[j][h];
+        }
+    }
+    __syncthreads();
+    if (tid < kBigBN && colmap[tid] >= 0) {
+      double sl = 0.0, sc = 0.0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        sl += epi_red[0][w][tid];
+        sc += epi_red[1][w][tid];
+      }
+      g.part_loss[(size_t)blockIdx.x * g.part_ld + colmap[tid]] = sl;
+      g.part_conj[(size_t)blockIdx.x * g.part_ld + colmap[tid]] = sc;
+    }
+  }
+}
+
+}  // namespace bnbg

@@ -1,4 +1,5 @@
 // gemm_kernels.cu -- instantiations and launcher of the DMMA GEMM kernels.
+#include "gemm_big.cuh"
 #include "launchers.hpp"
 
 namespace bnbg {
@@ -21,7 +22,32 @@ cudaError_t gemm_set_attrs() {
   if (e == cudaSuccess) e = set_attr<true, FM, FN, EPI_STORE>();
   FOR_GEMM_CFGS(SETA)
 #undef SETA
+  const int big = (int)kBigSmemBytes;
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_gemm_big<false, EPI_DERIV>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_gemm_big<false, EPI_EVAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_gemm_big<false, EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_gemm_big<true, EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   return e;
+}
+
+int gemm_big_tile_m() { return kBigBM; }
+int gemm_big_tile_n() { return kBigBN; }
+
+cudaError_t gemm_big_launch(bool tn, int epi, dim3 grid, cudaStream_t st, const GemmArgs& g) {
+  const dim3 block(kBigThreads);
+  if (tn)
+    k_gemm_big<true, EPI_STORE><<<grid, block, kBigSmemBytes, st>>>(g);
+  else if (epi == EPI_DERIV)
+    k_gemm_big<false, EPI_DERIV><<<grid, block, kBigSmemBytes, st>>>(g);
+  else if (epi == EPI_EVAL)
+    k_gemm_big<false, EPI_EVAL><<<grid, block, kBigSmemBytes, st>>>(g);
+  else
+    k_gemm_big<false, EPI_STORE><<<grid, block, kBigSmemBytes, st>>>(g);
+  return cudaGetLastError();
 }
 
 cudaError_t gemm_launch(bool tn, int epi, int fm, int fn, dim3 grid, cudaStream_t st,

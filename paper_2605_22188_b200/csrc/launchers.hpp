@@ -47,6 +47,10 @@ struct PassArgs {
 cudaError_t gemm_set_attrs();
 cudaError_t gemm_launch(bool tn, int epi, int fm, int fn, dim3 grid, cudaStream_t st,
                         const GemmArgs& g);
+// register-tiled 128 x 64 DMMA GEMM for wide batches (gemm_big.cuh); n, p even
+int gemm_big_tile_m();
+int gemm_big_tile_n();
+cudaError_t gemm_big_launch(bool tn, int epi, dim3 grid, cudaStream_t st, const GemmArgs& g);
 
 // ---- column_kernels.cu -----------------------------------------------------
 int column_E(int n2);  // register-sort elements per thread (0: shared-memory sort)
