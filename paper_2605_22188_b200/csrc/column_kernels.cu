@@ -3,6 +3,8 @@
 
 namespace bnbg {
 
+// E = 8 (p <= 2048) was measured slower than the shared-memory network: the
+// 2048-key network does not unroll and its arrays land in local memory
 int column_E(int n2) { return n2 <= 256 ? 1 : n2 <= 512 ? 2 : n2 <= 1024 ? 4 : 0; }
 
 #define DISPATCH_E(E_, ...)  \

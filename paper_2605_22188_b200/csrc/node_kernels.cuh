@@ -16,7 +16,7 @@
 // t holds E consecutive elements, strides below E are register swaps, strides
 // below 32E are warp shuffles, and only the cross-warp strides go through
 // shared memory (6 barriers for 512 keys instead of 45).  E = 0 selects the
-// shared-memory network for p > 2048.  Every reduction has a fixed
+// shared-memory network for p > 1024.  Every reduction has a fixed
 // association order (deterministic results).
 #pragma once
 #include "device_math.cuh"

@@ -1,0 +1,38 @@
+// pass_impl.cuh -- definitions behind pass_impl.hpp (included by pass_e<E>.cu).
+#pragma once
+#include "pass_impl.hpp"
+#include "pass_kernel.cuh"
+
+namespace bnbg {
+
+template <int E>
+cudaError_t pass_static_smem_t(size_t* bytes) {
+  cudaFuncAttributes fa;
+  const cudaError_t e = cudaFuncGetAttributes(&fa, k_pass<E>);
+  *bytes = e == cudaSuccess ? fa.sharedSizeBytes : 0;
+  return e;
+}
+
+template <int E>
+cudaError_t pass_setup_t(size_t smem, int* blocks_per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(k_pass<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_pass<E>, kPassThreads, smem);
+  return e;
+}
+
+template <int E>
+cudaError_t pass_launch_t(int grid, size_t smem, cudaStream_t st, PassArgs* a) {
+  void* args[] = {a};
+  return cudaLaunchCooperativeKernel((const void*)k_pass<E>, dim3(grid), dim3(kPassThreads), args,
+                                     smem, st);
+}
+
+}  // namespace bnbg
+
+#define BNBG_INSTANTIATE_PASS(E)                                                            \
+  namespace bnbg {                                                                          \
+  template cudaError_t pass_static_smem_t<E>(size_t*);                                      \
+  template cudaError_t pass_setup_t<E>(size_t, int*);                                       \
+  template cudaError_t pass_launch_t<E>(int, size_t, cudaStream_t, PassArgs*);              \
+  }

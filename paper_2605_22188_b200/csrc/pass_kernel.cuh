@@ -140,7 +140,7 @@ __host__ __device__ inline size_t res_work_doubles(const ResLayout& r) {
 }
 
 // Loads this CTA's resident tiles of X (once per pass).
-__device__ void res_load_x(const PassArgs& a, double* smem) {
+static __device__ void res_load_x(const PassArgs& a, double* smem) {
   const ResLayout& L = a.res;
   const double* X = a.nn.A;
   const int n = a.n, p = a.p;
@@ -323,7 +323,7 @@ __device__ void res_phase_nn(const PassArgs& a, const double* Bsrc, int ma, doub
   }
 }
 
-__device__ void res_phase_tn(const PassArgs& a, int ma, double* smem, int* colmap,
+static __device__ void res_phase_tn(const PassArgs& a, int ma, double* smem, int* colmap,
                              const int* act) {
   const ResLayout& L = a.res;
   if ((int)blockIdx.x >= L.tn_mt * L.tn_split) return;

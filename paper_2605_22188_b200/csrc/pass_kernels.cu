@@ -1,6 +1,9 @@
-// pass_kernels.cu -- instantiations and cooperative launcher of k_pass.
+// pass_kernels.cu -- host dispatch of the persistent pass kernel over the
+// column-sort width E.  Each k_pass<E> instantiation lives in its own
+// translation unit (pass_e<E>.cu) so the five compile in parallel.
 #include "launchers.hpp"
 #include "pass_kernel.cuh"
+#include "pass_impl.hpp"
 
 namespace bnbg {
 
@@ -64,29 +67,20 @@ size_t pass_res_plan(int n, int p, int n2, int E, int grid, size_t smem_limit, R
 
 cudaError_t pass_static_smem(int E, size_t* bytes) {
   cudaError_t e = cudaSuccess;
-  cudaFuncAttributes fa;
-  DISPATCH_E(E, e = cudaFuncGetAttributes(&fa, k_pass<EV>));
-  *bytes = e == cudaSuccess ? fa.sharedSizeBytes : 0;
+  DISPATCH_E(E, e = pass_static_smem_t<EV>(bytes));
   return e;
 }
 
 cudaError_t pass_setup(int E, size_t smem, int* blocks_per_sm) {
   cudaError_t e = cudaSuccess;
   *blocks_per_sm = 0;
-  DISPATCH_E(E, {
-    e = cudaFuncSetAttribute(k_pass<EV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_pass<EV>, kPassThreads,
-                                                        smem);
-  });
+  DISPATCH_E(E, e = pass_setup_t<EV>(smem, blocks_per_sm));
   return e;
 }
 
 cudaError_t pass_launch(int E, int grid, size_t smem, cudaStream_t st, PassArgs* a) {
-  void* args[] = {a};
   cudaError_t e = cudaSuccess;
-  DISPATCH_E(E, e = cudaLaunchCooperativeKernel((const void*)k_pass<EV>, dim3(grid),
-                                                dim3(kPassThreads), args, smem, st));
+  DISPATCH_E(E, e = pass_launch_t<EV>(grid, smem, st, a));
   return e;
 }
 

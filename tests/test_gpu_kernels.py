@@ -191,6 +191,29 @@ def test_relax_batch_matches_oracle(bnb, orc, loss, n, p, k, m):
                                    atol=1e-6)
 
 
+@pytest.mark.parametrize("loss,n,p,k,m,its", [
+    (0, 200, 40, 4, 300, 40),     # m > 2 x SMs: multi-kernel path, 128 x 64 register-tiled GEMM
+    (1, 240, 60, 5, 320, 30),
+    (0, 1200, 1100, 6, 5, 30),    # p in (1024, 2048]: 8-wide register column sort
+    (1, 900, 1500, 7, 4, 20),
+])
+def test_relax_batch_wide_and_large_p(bnb, orc, loss, n, p, k, m, its):
+    """Parity of the c3/c4 code paths at oracle-affordable sizes (capped iterations)."""
+    inst, eng = _engine(bnb, orc, n, p, k, 0.7, loss, seed=5)
+    rng = np.random.default_rng(n * p + m)
+    st, kb = rnd_batch(rng, p, m, k, all_free_first=True)
+    warm = np.zeros((p, m))
+    L = orc.smoothness(loss, inst.X)
+    res = eng.solve_batch_relaxation((st, kb, warm),
+                                     bnb.RelaxConfig(smoothness=L, max_iterations=its), math.inf)
+    ob, obnd, ost, oit = orc.relax_batch(inst, st, kb, warm, math.inf,
+                                         orc.relax_cfg(smoothness=L, max_iterations=its))
+    np.testing.assert_allclose(res.bounds, obnd, rtol=1e-6, atol=1e-6)
+    assert res.status.tolist() == ost.tolist()
+    assert res.iterations.tolist() == oit.tolist()
+    np.testing.assert_allclose(res.beta, ob, rtol=1e-6, atol=1e-7)
+
+
 def test_relax_frozen_columns_bit_stable_and_batch_of_one(bnb, orc):
     """batch-of-m equals m independent single-node solves."""
     inst, eng = _engine(bnb, orc, 400, 50, 4, 0.6, 0, seed=5)
