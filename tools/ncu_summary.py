@@ -28,6 +28,9 @@ METRICS = {
     "launch__registers_per_thread": "registers",
     "launch__shared_mem_per_block_dynamic": "dyn_smem",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
+    "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active": "dmma_pipe_pct",
+    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed":
+        "tensor_pipe_elapsed_pct",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Kbyte/block": 1e3,
          "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0, "nsecond": 1e-9, "usecond": 1e-6,
