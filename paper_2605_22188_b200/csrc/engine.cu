@@ -368,17 +368,25 @@ int Engine::compute_smoothness(double* out) {
     const double nv = vnorm(v);
     for (double& x : v) x /= nv;
   }
-  if (int rc = ensure_aux(sizeof(double) * ((size_t)2 * p + n + 2))) return rc;
+  // X v over column chunks: enough CTAs for the SMs even when n is small
+  const int row_blocks = (n + 255) / 256;
+  int nsplit = std::max(1, std::min(32, (2 * sms_ + row_blocks - 1) / row_blocks));
+  const int chunk = (p + nsplit - 1) / nsplit;
+  nsplit = (p + chunk - 1) / chunk;
+  if (int rc = ensure_aux(sizeof(double) * ((size_t)2 * p + n + 2 + (size_t)nsplit * n))) return rc;
   double* dv = static_cast<double*>(dAux_);
   double* dw = dv + p;
   double* dxv = dw + p;
   double* dstat = dxv + n;
+  double* dpart = dstat + 2;
   if (int rc_ = h2d(dv, v.data(), sizeof(double) * p)) return rc_;
   double estimate = 0.0, stats[2];
   double result = -1.0;
   for (int it = 0; it < 100; ++it) {
-    k_gemv_n<<<(n + 255) / 256, 256, 0, stream_>>>(n, p, dX_, dv, dxv);
-    CKL("k_gemv_n");
+    k_gemv_n_part<<<dim3(row_blocks, nsplit), 256, 0, stream_>>>(n, p, chunk, dX_, dv, dpart);
+    CKL("k_gemv_n_part");
+    k_gemv_n_sum<<<row_blocks, 256, 0, stream_>>>(n, nsplit, dpart, dxv);
+    CKL("k_gemv_n_sum");
     k_gemv_t<<<(p + 7) / 8, 256, 0, stream_>>>(n, p, dX_, dxv, dw);
     CKL("k_gemv_t");
     k_power_stats<<<1, 256, 0, stream_>>>(p, dv, dw, dstat);

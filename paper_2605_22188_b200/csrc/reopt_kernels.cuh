@@ -2,7 +2,7 @@
 //
 //   k_reopt / k_reopt_direct / k_reopt_gram   reoptimize_supports
 //                                  (primal_heuristics.hpp:174-227)
-//   k_gemv_n / k_gemv_t / k_power_stats / k_scale   smoothness_constant
+//   k_gemv_n_part / _sum, k_gemv_t, k_power_stats, k_scale   smoothness_constant
 //                                  power iteration (losses.hpp:86-112)
 #pragma once
 #include <cooperative_groups.h>
@@ -472,14 +472,27 @@ static __global__ void __launch_bounds__(kReoptFastThreads)
 // --------------------------------------------------------------------------
 // smoothness constant (losses.hpp:86-112): power-iteration GEMVs
 // --------------------------------------------------------------------------
-static __global__ void k_gemv_n(int n, int p, const double* __restrict__ X, const double* __restrict__ v,
-                         double* __restrict__ xv) {
+// X v split over column chunks (grid.y): partial[s*n + i] over chunk s, summed
+// in chunk order by k_gemv_n_sum -- enough CTAs to cover the SMs at c2 sizes
+static __global__ void k_gemv_n_part(int n, int p, int chunk, const double* __restrict__ X,
+                                     const double* __restrict__ v, double* __restrict__ part) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const int j0 = blockIdx.y * chunk, j1 = min(p, j0 + chunk);
   double s = 0.0;
-  for (int j = 0; j < p; ++j) s += X[(size_t)j * n + i] * v[j];
+  for (int j = j0; j < j1; ++j) s += X[(size_t)j * n + i] * v[j];
+  part[(size_t)blockIdx.y * n + i] = s;
+}
+
+static __global__ void k_gemv_n_sum(int n, int ns, const double* __restrict__ part,
+                                    double* __restrict__ xv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = part[i];
+  for (int q = 1; q < ns; ++q) s += part[(size_t)q * n + i];
   xv[i] = s;
 }
+
 
 static __global__ void k_gemv_t(int n, int p, const double* __restrict__ X, const double* __restrict__ xv,
                          double* __restrict__ w) {
