@@ -1,4 +1,6 @@
 // reopt_kernels.cu -- instantiations and cluster launcher of k_reopt_cluster.
+#include <cstdlib>
+
 #include "launchers.hpp"
 #include "reopt_kernels.cuh"
 
@@ -21,6 +23,13 @@ static cudaError_t launch_q_r(int cs, int nsup, cudaStream_t st, int n, const do
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  static const bool mb = [] {
+    const char* e = getenv("BNBG_REOPT_MB");  // 0: cluster-barrier exchange
+    return !(e && e[0] == '0');
+  }();
+  if (mb)
+    return cudaLaunchKernelEx(&cfg, k_reopt_cluster_mb<Q, R>, n, X, y, loss, M, lambda2, step, off,
+                              idx, coef, obj, its);
   return cudaLaunchKernelEx(&cfg, k_reopt_cluster<Q, R>, n, X, y, loss, M, lambda2, step, off, idx,
                             coef, obj, its);
 }

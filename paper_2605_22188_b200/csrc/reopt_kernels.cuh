@@ -365,6 +365,185 @@ __global__ void __launch_bounds__(kReoptClusterThreads)
   }
 }
 
+// k_reopt_cluster_mb: k_reopt_cluster with the per-iteration exchange done by
+// st.async remote stores that complete transactions on the receiver's
+// mbarrier (double-buffered), instead of a full cluster barrier: a CTA waits
+// only for the bytes it needs, with no cluster-wide arrive/wait round trip.
+// A buffer's barrier is re-armed (arrive.expect_tx) after the next iteration's
+// first block barrier -- every thread has consumed it by then -- and before
+// this CTA's sends of that iteration, which precede every sender's next write
+// to it: one block barrier per iteration.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ uint32_t cluster_map(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_f64(uint32_t addr, double v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(
+                   addr),
+               "l"(__double_as_longlong(v)), "r"(bar)
+               : "memory");
+}
+
+template <int QMAX, int RPT>
+__global__ void __launch_bounds__(kReoptClusterThreads)
+    k_reopt_cluster_mb(int n, const double* __restrict__ X, const double* __restrict__ y, int loss,
+                       double M, double lambda2, double step, const int* off, const int* sidx,
+                       double* coef_out, double* obj_out, int* it_out) {
+  namespace cg = cooperative_groups;
+  constexpr int NT = kReoptClusterThreads, NW = NT / 32;
+  cg::cluster_group cl = cg::this_cluster();
+  const int CS = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  const int s = blockIdx.x / CS;
+  __shared__ double red[2][NW][QMAX];
+  __shared__ __align__(16) double xsum[2][kReoptMaxCluster][QMAX];
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ double fin[kReoptMaxCluster];
+  __shared__ double wred[NW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = off[s + 1] - off[s];
+  const int* S = sidx + off[s];
+  const int chunk = (n + CS - 1) / CS;
+  const int r0 = rank * chunk, r1 = min(n, r0 + chunk);
+  const uint32_t bytes = (uint32_t)(CS * QMAX * sizeof(double));
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    mbar_arm(&mbar[0], bytes);
+    mbar_arm(&mbar[1], bytes);
+  }
+  double xs[RPT][QMAX], ys[RPT];
+  bool valid[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int i = r0 + j * NT + tid;
+    valid[j] = i < r1;
+    ys[j] = valid[j] ? y[i] : 0.0;
+#pragma unroll
+    for (int r = 0; r < QMAX; ++r) xs[j][r] = (valid[j] && r < q) ? X[(size_t)S[r] * n + i] : 0.0;
+  }
+  cl.sync();  // barriers initialised and armed everywhere before any remote store
+  // this CTA's slot in every receiver, and every receiver's barrier, as
+  // shared::cluster addresses
+  uint32_t dst_slot = 0, dst_bar = 0;
+  const int my_dst = tid / QMAX, my_r = tid % QMAX;
+  if (tid < CS * QMAX) {
+    dst_slot = cluster_map(smem_addr(&xsum[0][rank][my_r]), (uint32_t)my_dst);
+    dst_bar = cluster_map(smem_addr(&mbar[0]), (uint32_t)my_dst);
+  }
+  const uint32_t buf_stride = (uint32_t)(kReoptMaxCluster * QMAX * sizeof(double));
+  double beta[QMAX];
+#pragma unroll
+  for (int r = 0; r < QMAX; ++r) beta[r] = 0.0;
+  const int ridx = reduce_scatter_index<QMAX>(lane);
+  const bool writer = (lane & (32 / QMAX - 1)) == 0;
+  int its = 0;
+  if (q > 0) {
+    for (int it = 0; it < 5000; ++it) {
+      ++its;
+      const int buf = it & 1;
+      double part[QMAX];
+#pragma unroll
+      for (int r = 0; r < QMAX; ++r) part[r] = 0.0;
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        double sc = 0.0;  // scores, r ascending (primal_heuristics.hpp:194-198)
+#pragma unroll
+        for (int r = 0; r < QMAX; ++r) sc += beta[r] * xs[j][r];
+        const double di = valid[j] ? d_loss_deriv(loss, sc, ys[j]) : 0.0;
+#pragma unroll
+        for (int r = 0; r < QMAX; ++r) part[r] += xs[j][r] * di;
+      }
+      warp_reduce_scatter<QMAX>(part, lane);
+      if (writer) red[buf][warp][ridx] = part[0];
+      __syncthreads();
+      // every thread has finished reading the other buffer (last iteration):
+      // re-arm it for its next use, before this CTA's sends of this iteration
+      if (tid == 0 && it > 0) mbar_arm(&mbar[buf ^ 1], bytes);
+      if (tid < CS * QMAX) {
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) v += red[buf][w][my_r];
+        st_async_f64(dst_slot + buf * buf_stride, v, dst_bar + buf * (uint32_t)sizeof(uint64_t));
+      }
+      mbar_wait(&mbar[buf], (uint32_t)((it >> 1) & 1));
+      double gs[QMAX];
+#pragma unroll
+      for (int r = 0; r < QMAX; ++r) gs[r] = 0.0;
+      for (int c = 0; c < CS; ++c) {
+        const double2* row = reinterpret_cast<const double2*>(xsum[buf][c]);
+#pragma unroll
+        for (int r2 = 0; r2 < QMAX / 2; ++r2) {
+          const double2 t = row[r2];
+          gs[2 * r2] += t.x;
+          gs[2 * r2 + 1] += t.y;
+        }
+      }
+      double gm2 = 0.0;
+#pragma unroll
+      for (int r = 0; r < QMAX; ++r) {
+        double g = gs[r];
+        g += 2.0 * lambda2 * beta[r];  // (:210-211)
+        double v = beta[r] - step * g;
+        v = v < -M ? -M : v;
+        v = v > M ? M : v;
+        const double dl = beta[r] - v;
+        gm2 += dl * dl;
+        beta[r] = r < q ? v : 0.0;
+      }
+      if (sqrt(gm2) / step <= 1e-8) break;  // (:212-215)
+    }
+  }
+  // objective lambda2 |beta|^2 + sum l(X_S beta)  (:217-222)
+  double acc = 0.0;
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    double sc = 0.0;
+#pragma unroll
+    for (int r = 0; r < QMAX; ++r) sc += beta[r] * xs[j][r];
+    if (valid[j]) acc += d_loss_value(loss, sc, ys[j]);
+  }
+  const double cta = block_sum<NT>(acc, wred);
+  if (tid == 0) *cl.map_shared_rank(&fin[rank], 0) = cta;
+  cl.sync();
+  if (rank == 0 && tid == 0) {
+    double sq = 0.0;
+#pragma unroll
+    for (int r = 0; r < QMAX; ++r) sq += beta[r] * beta[r];
+    double obj = lambda2 * sq;
+    for (int c = 0; c < CS; ++c) obj += fin[c];
+    obj_out[s] = obj;
+    if (it_out) it_out[s] = its;
+    for (int r = 0; r < q && r < QMAX; ++r) coef_out[off[s] + r] = beta[r];
+  }
+}
+
 // k_reopt_gram (squared loss): X_S'(X_S beta - y) = Gram beta - X_S'y, the
 // same iterates in exact arithmetic.  The q x q Gram and
 // X_S'y are built once per support; warp 0 then runs the projected-gradient
