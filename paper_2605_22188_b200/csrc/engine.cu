@@ -598,6 +598,13 @@ int Engine::run_pass(int m, const RelaxParams& cfg, double thr, double eta, doub
   a.tn.probe = dPassProf_ ? dPassProf_ + 24 : nullptr;
   a.bar = dBar_;
   a.res = res_;
+  {
+    static const bool big_ok = [] {
+      const char* e = getenv("BNBG_BIGGEMM");
+      return !(e && e[0] == '0');
+    }();
+    a.big = big_ok && (n % 2) == 0 && (p % 2) == 0;
+  }
   CK(cudaMemsetAsync(dBar_, 0, sizeof(unsigned), stream_));
   tic(KC_PASS);
   cudaError_t e = cudaSuccess;

@@ -24,15 +24,14 @@ constexpr int kBigB = kBigBN * kBigLDK;
 constexpr int kBigStage = kBigA + kBigB;
 constexpr size_t kBigSmemBytes = sizeof(double) * (size_t)kBigNS * kBigStage;
 
+// One 128 x 64 output tile (row tile mt, column tile nt).  All 256 threads of
+// the CTA call; smem holds kBigSmemBytes; colmap kBigBN ints and epi_red
+// 2 x 4 x kBigBN doubles of shared memory.  Ends with a block barrier.
 template <bool TN, int EPI>
-__global__ void __launch_bounds__(kBigThreads, 2) k_gemm_big(GemmArgs g) {
-  extern __shared__ __align__(16) double smem[];
-  __shared__ int colmap[kBigBN];
-  __shared__ double epi_red[2][4][kBigBN];  // EVAL: per-warp-row column sums (l, l*)
-  const int ncols = *g.d_ncols;
-  const int n0 = blockIdx.y * kBigBN;
-  if (n0 >= ncols) return;
-  const int m0 = blockIdx.x * kBigBM;
+__device__ void gemm_big_tile(const GemmArgs& g, int ncols, int mt, int nt, double* smem,
+                              int* colmap, double (*epi_red)[4][kBigBN]) {
+  const int n0 = nt * kBigBN;
+  const int m0 = mt * kBigBM;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 3, wn = warp >> 2;
   if (tid < kBigBN) {
@@ -171,10 +170,21 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_gemm_big(GemmArgs g) {
         sl += epi_red[0][w][tid];
         sc += epi_red[1][w][tid];
       }
-      g.part_loss[(size_t)blockIdx.x * g.part_ld + colmap[tid]] = sl;
-      g.part_conj[(size_t)blockIdx.x * g.part_ld + colmap[tid]] = sc;
+      g.part_loss[(size_t)mt * g.part_ld + colmap[tid]] = sl;
+      g.part_conj[(size_t)mt * g.part_ld + colmap[tid]] = sc;
     }
   }
+  __syncthreads();  // smem / colmap reusable by the caller's next tile
+}
+
+template <bool TN, int EPI>
+__global__ void __launch_bounds__(kBigThreads, 2) k_gemm_big(GemmArgs g) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int colmap[kBigBN];
+  __shared__ double epi_red[2][4][kBigBN];  // EVAL: per-warp-row column sums (l, l*)
+  const int ncols = *g.d_ncols;
+  if ((int)blockIdx.y * kBigBN >= ncols) return;
+  gemm_big_tile<TN, EPI>(g, ncols, blockIdx.x, blockIdx.y, smem, colmap, epi_red);
 }
 
 }  // namespace bnbg

@@ -41,6 +41,8 @@ struct PassArgs {
   unsigned long long* prof;  // optional phase wall times (ns, CTA 0's view); nullptr: off
   unsigned* bar;             // grid barrier counter (zeroed before the launch)
   ResLayout res;
+  int big;                   // streaming mode: 128 x 64 register-tiled GEMM tiles when
+                             // m_a >= 64 (gemm_big.cuh; needs n, p even)
 };
 
 // ---- gemm_kernels.cu -------------------------------------------------------

@@ -35,6 +35,7 @@
 #include <cooperative_groups.h>
 
 #include "gemm.cuh"
+#include "gemm_big.cuh"
 #include "launchers.hpp"
 #include "node_kernels.cuh"
 
@@ -61,12 +62,22 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target) {
 // ---------------------------------------------------------------------------
 // streaming-mode phases
 // ---------------------------------------------------------------------------
+// streaming mode uses the 128 x 64 register-tiled GEMM tiles for wide batches
+__device__ __forceinline__ bool pass_big(const PassArgs& a, int ma) { return a.big && ma >= 64; }
+
 template <int EPI>
 __device__ void pass_phase_nn(const PassArgs& a, const double* Bsrc, int ma, double* smem,
                               int* colmap, const int* act) {
   GemmArgs g = a.nn;
   g.B = Bsrc;
   g.act = act;
+  if (pass_big(a, ma)) {
+    const int mt = (a.n + kBigBM - 1) / kBigBM, nt = (ma + kBigBN - 1) / kBigBN;
+    auto* epi = reinterpret_cast<double(*)[4][kBigBN]>(smem + kBigSmemBytes / sizeof(double));
+    for (int t = blockIdx.x; t < mt * nt; t += gridDim.x)
+      gemm_big_tile<false, EPI>(g, ma, t % mt, t / mt, smem, colmap, epi);
+    return;
+  }
   const int fn = pass_fn(ma);
   const int mt = (a.n + 15) / 16;
   const int nt = (ma + 8 * fn - 1) / (8 * fn);
@@ -86,6 +97,13 @@ __device__ inline int pass_phase_tn(const PassArgs& a, int ma, double* smem, int
                                     const int* act) {
   GemmArgs g = a.tn;
   g.act = act;
+  if (pass_big(a, ma)) {
+    const int mt = (a.p + kBigBM - 1) / kBigBM, nt = (ma + kBigBN - 1) / kBigBN;
+    auto* epi = reinterpret_cast<double(*)[4][kBigBN]>(smem + kBigSmemBytes / sizeof(double));
+    for (int t = blockIdx.x; t < mt * nt; t += gridDim.x)
+      gemm_big_tile<true, EPI_STORE>(g, ma, t % mt, t / mt, smem, colmap, epi);
+    return 1;
+  }
   const int fn = pass_fn(ma);
   const int mt = (a.p + 15) / 16;
   const int nt = (ma + 8 * fn - 1) / (8 * fn);
@@ -115,8 +133,10 @@ __host__ inline size_t pass_smem_bytes(int p, int n2, int E) {
   size_t b = column_smem_bytes(p, n2, E);
   const size_t g1 = GemmShape<false, 2, 4, kPassNW>::SMEM_BYTES;
   const size_t g2 = GemmShape<true, 2, 4, kPassNW>::SMEM_BYTES;
+  const size_t g3 = kBigSmemBytes + sizeof(double) * 2 * 4 * kBigBN;  // big tiles + epilogue sums
   if (g1 > b) b = g1;
   if (g2 > b) b = g2;
+  if (g3 > b) b = g3;
   return b;
 }
 
@@ -357,7 +377,7 @@ constexpr int kActCache = 256;
 template <int E>
 __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant__ PassArgs a) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ int colmap[32];
+  __shared__ int colmap[kBigBN];  // column map of the current GEMM tile (<= 64 columns)
   __shared__ int s_act[kActCache];  // the active list, refreshed after every compaction
   const RelaxDev& r = a.r;  // kernel-parameter space (no local copy)
   int nsplit = 1;            // split-K slabs of the current G
@@ -445,7 +465,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
     EvalArgs e;
     e.part_loss = a.nn.part_loss;
     e.part_conj = a.nn.part_conj;
-    e.nrb = (a.n + 15) / 16;
+    e.nrb = !res && pass_big(a, ma) ? (a.n + kBigBM - 1) / kBigBM : (a.n + 15) / 16;
     e.part_ld = a.nn.part_ld;
     e.iter = it;
     e.prune_threshold = a.prune_thr;
