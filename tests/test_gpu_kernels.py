@@ -163,6 +163,25 @@ def test_reopt_matches_oracle(bnb, orc, loss):
         np.testing.assert_allclose(a, b, rtol=1e-6, atol=1e-8)
 
 
+@pytest.mark.parametrize("n,sizes", [(2000, [3, 8, 5]),        # registers, 8-wide
+                                     (3000, [12, 9, 16]),      # registers, 16-wide
+                                     (5000, [12, 15, 10]),     # large n: per-CTA gather form
+                                     (9000, [7, 3])])
+def test_reopt_cluster_paths_match_oracle(bnb, orc, n, sizes):
+    """Logistic re-optimisation through each kernel variant (cluster register
+    slices while a support's rows fit 8 CTAs' registers, else the gather form)."""
+    p = 40
+    inst, eng = _engine(bnb, orc, n, p, 16, 0.7, 1)
+    rng = np.random.default_rng(n)
+    sups = [list(rng.choice(p, q, replace=False)) for q in sizes]
+    r = eng.reoptimize_supports(sups)
+    oc, oo = orc.reoptimize(inst, sups, orc.smoothness(1, inst.X))
+    for a, b in zip(r.objectives, oo):
+        assert abs(a - b) <= 1e-9 * max(1, abs(b))
+    for a, b in zip(r.coefficients, oc):
+        np.testing.assert_allclose(a, b, rtol=1e-6, atol=1e-8)
+
+
 @pytest.mark.parametrize("loss,n,p,k,m", [(0, 1000, 100, 5, 12), (1, 2000, 500, 8, 6),
                                           (0, 300, 64, 4, 40), (1, 150, 30, 3, 9)])
 def test_relax_batch_matches_oracle(bnb, orc, loss, n, p, k, m):
