@@ -157,6 +157,16 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
     }
   }
   nrb_max_ = (n + 15) / 16;
+  // batch workspaces and the node pool sized for a typical narrow frontier up
+  // front, so the first passes of a solve do not pay cudaMalloc/cudaFree
+  // (cudaFree synchronises the device) while the batch width grows
+  {
+    const size_t col_bytes = (size_t)p * 40 + (size_t)n * 8;
+    const int pre = (int)std::min<size_t>(128, std::max<size_t>(16, (256u << 20) / col_bytes));
+    if (int rc = ensure(pre)) return rc;
+    if (int rc = ensure_pool_batch(pre)) return rc;
+    if (int rc = pool_reserve(4 * pre)) return rc;
+  }
   CK(cudaStreamSynchronize(stream_));
   if (L_ > 0.0) {
     L = L_;
