@@ -217,8 +217,11 @@ def main():
     import paper_2605_22188_b200 as P
 
     torch.cuda.set_device(local)
+    # BNBG_BENCH_SHARDED=1 runs the node-sharded path even at one rank (under
+    # torchrun, NCCL world size 1) -- a check of the N > 1 code path on one GPU
+    sharded = world > 1 or os.environ.get("BNBG_BENCH_SHARDED") == "1"
     dist = None
-    if world > 1:
+    if sharded:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n, p, k, rho, loss, desc = spec
@@ -231,7 +234,7 @@ def main():
     def certify(engine):
         if args.config == "c5":  # collect_rashomon (rashomon.hpp:149-218): same hot path
             return engine.collect_rashomon(cfg, P.RashomonConfig(epsilon=0.01)).certificate
-        return engine.solve_sharded(cfg, transport="nccl") if world > 1 else engine.solve(cfg)
+        return engine.solve_sharded(cfg, transport="nccl") if sharded else engine.solve(cfg)
 
     for _ in range(args.warmup):
         certify(eng)
@@ -345,7 +348,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps,
-            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "higher_is_better": True, "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (generate_synthetic, seed 0, problem.hpp:70-132)",
             "config": {"workload": f"{args.config}: {desc}, " + (
@@ -353,7 +356,7 @@ def main():
                            else f"nodes/s within a {args.time_limit:g} s time limit"),
                        "n": n, "p": p, "k": k, "rho": rho, "loss": "logistic" if loss else "squared",
                        "batch_size": c0.batch_size_used,
-                       "parallelism": f"node-sharded over {world} GPUs (NCCL)" if world > 1
+                       "parallelism": f"node-sharded over {world} GPUs (NCCL)" if sharded
                        else "single GPU",
                        "l2": "flushed (256 MiB write) before every step",
                        "time_to_certify_s": total_ms_max / args.steps / 1e3,

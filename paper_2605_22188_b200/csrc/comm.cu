@@ -42,26 +42,26 @@ static PoolDev pool_view2(void* const* mem, int p, int k, int cap) {
 
 size_t Engine::node_record_bytes() const { return node_rec_bytes(p, std::max(k, 1)); }
 
-static int grow(void** ptr, size_t* cap, size_t want) {
+static int grow(void** ptr, size_t* cap, size_t want, cudaStream_t st) {
   if (want <= *cap) return 0;
-  cudaFree(*ptr);
+  if (*ptr) cudaFreeAsync(*ptr, st);
   *ptr = nullptr;
   const size_t c = std::max(want, *cap * 2);
-  if (cudaMalloc(ptr, c) != cudaSuccess) return 1;
+  if (cudaMallocAsync(ptr, c, st) != cudaSuccess) return 1;
   *cap = c;
   return 0;
 }
 
 int Engine::pool_pack(int cnt, const int* slots, const double* lbs, uint8_t** d_send) {
   const size_t rb = node_record_bytes();
-  if (grow(reinterpret_cast<void**>(&dXSend_), &xsend_bytes_, std::max<size_t>(rb * cnt, 64)))
+  if (grow(reinterpret_cast<void**>(&dXSend_), &xsend_bytes_, std::max<size_t>(rb * cnt, 64), stream_))
     return fail(4, "node exchange: out of device memory");
   if (cnt > xslots_cap_) {
-    cudaFree(dXSlots_);
-    cudaFree(dXLb_);
+    dfree(dXSlots_);
+    dfree(dXLb_);
     xslots_cap_ = std::max(cnt, 2 * xslots_cap_);
-    CK(cudaMalloc(&dXSlots_, sizeof(int) * xslots_cap_));
-    CK(cudaMalloc(&dXLb_, sizeof(double) * xslots_cap_));
+    CK(cudaMallocAsync(&dXSlots_, sizeof(int) * xslots_cap_, stream_));
+    CK(cudaMallocAsync(&dXLb_, sizeof(double) * xslots_cap_, stream_));
   }
   *d_send = dXSend_;
   if (cnt <= 0) return 0;
@@ -76,7 +76,7 @@ int Engine::pool_pack(int cnt, const int* slots, const double* lbs, uint8_t** d_
 
 int Engine::pool_recv_buffer(int cnt, uint8_t** d_recv) {
   const size_t rb = node_record_bytes();
-  if (grow(reinterpret_cast<void**>(&dXRecv_), &xrecv_bytes_, std::max<size_t>(rb * cnt, 64)))
+  if (grow(reinterpret_cast<void**>(&dXRecv_), &xrecv_bytes_, std::max<size_t>(rb * cnt, 64), stream_))
     return fail(4, "node exchange: out of device memory");
   *d_recv = dXRecv_;
   return 0;
@@ -85,11 +85,11 @@ int Engine::pool_recv_buffer(int cnt, uint8_t** d_recv) {
 int Engine::pool_unpack(int cnt, const int* slots, double* lbs) {
   if (cnt <= 0) return 0;
   if (cnt > xslots_cap_) {
-    cudaFree(dXSlots_);
-    cudaFree(dXLb_);
+    dfree(dXSlots_);
+    dfree(dXLb_);
     xslots_cap_ = std::max(cnt, 2 * xslots_cap_);
-    CK(cudaMalloc(&dXSlots_, sizeof(int) * xslots_cap_));
-    CK(cudaMalloc(&dXLb_, sizeof(double) * xslots_cap_));
+    CK(cudaMallocAsync(&dXSlots_, sizeof(int) * xslots_cap_, stream_));
+    CK(cudaMallocAsync(&dXLb_, sizeof(double) * xslots_cap_, stream_));
   }
   if (int rc = h2d(dXSlots_, slots, sizeof(int) * cnt)) return rc;
   k_pool_unpack<<<cnt, 128, 0, stream_>>>(pool_view2(pool_mem_, p, k, pool_cap_), cnt, dXRecv_,
@@ -102,11 +102,11 @@ int Engine::pool_unpack(int cnt, const int* slots, double* lbs) {
 }
 
 void Engine::comm_release() {
-  cudaFree(dXSend_);
-  cudaFree(dXRecv_);
-  cudaFree(dXSlots_);
-  cudaFree(dXLb_);
-  cudaFree(dGather_);
+  dfree(dXSend_);
+  dfree(dXRecv_);
+  dfree(dXSlots_);
+  dfree(dXLb_);
+  dfree(dGather_);
   dXSend_ = dXRecv_ = nullptr;
   dXSlots_ = nullptr;
   dXLb_ = nullptr;
@@ -131,7 +131,7 @@ int Engine::nccl_init(const uint8_t* uid, int rank, int world) {
 int Engine::comm_allgather_nccl(const void* send, size_t bytes, void* recv) {
   if (!nccl_comm) return fail(1, "solve_sharded: no NCCL communicator (bnbg_nccl_init)");
   const size_t need = bytes * (nccl_world + 1);
-  if (grow(&dGather_, &gather_bytes_, need)) return fail(4, "allgather: out of device memory");
+  if (grow(&dGather_, &gather_bytes_, need, stream_)) return fail(4, "allgather: out of device memory");
   uint8_t* d_in = static_cast<uint8_t*>(dGather_);
   uint8_t* d_out = d_in + bytes;
   if (int rc = h2d(d_in, send, bytes)) return rc;

@@ -34,46 +34,46 @@ static int next_pow2(int v) {
 }
 
 Engine::~Engine() {
-  cudaFree(dX_);
-  cudaFree(dy_);
-  cudaFree(dB_);
-  cudaFree(dV_);
-  cudaFree(dG_);
-  cudaFree(dR_);
-  cudaFree(dPL_);
-  cudaFree(dPC_);
-  cudaFree(dT_);
-  cudaFree(dBest_);
-  cudaFree(dLast_);
-  cudaFree(dState_);
-  cudaFree(dFrozen_);
-  cudaFree(dKbar_);
-  cudaFree(dPf_);
-  cudaFree(dStatus_);
-  cudaFree(dIters_);
-  cudaFree(dAct_);
-  cudaFree(dMa_);
-  cudaFree(dErr_);
-  cudaFree(dSup_);
-  cudaFree(dLen_);
-  cudaFree(dJb_);
-  cudaFree(dAux_);
-  cudaFree(dPassOut_);
-  cudaFree(dPassProf_);
-  cudaFree(dBar_);
+  dfree(dX_);
+  dfree(dy_);
+  dfree(dB_);
+  dfree(dV_);
+  dfree(dG_);
+  dfree(dR_);
+  dfree(dPL_);
+  dfree(dPC_);
+  dfree(dT_);
+  dfree(dBest_);
+  dfree(dLast_);
+  dfree(dState_);
+  dfree(dFrozen_);
+  dfree(dKbar_);
+  dfree(dPf_);
+  dfree(dStatus_);
+  dfree(dIters_);
+  dfree(dAct_);
+  dfree(dMa_);
+  dfree(dErr_);
+  dfree(dSup_);
+  dfree(dLen_);
+  dfree(dJb_);
+  dfree(dAux_);
+  dfree(dPassOut_);
+  dfree(dPassProf_);
+  dfree(dBar_);
   comm_release();
-  for (void* q : pool_mem_) cudaFree(q);
-  cudaFree(dSlots_);
-  cudaFree(dLbIn_);
-  cudaFree(dLbOut_);
-  cudaFree(dPos_);
-  cudaFree(dTot_);
-  cudaFree(dFree_);
-  cudaFree(dRec_);
-  cudaFree(dRecLb_);
-  cudaFree(dOneLen_);
-  cudaFree(dOneIdx_);
-  cudaFree(dLists_);
+  for (void* q : pool_mem_) dfree(q);
+  dfree(dSlots_);
+  dfree(dLbIn_);
+  dfree(dLbOut_);
+  dfree(dPos_);
+  dfree(dTot_);
+  dfree(dFree_);
+  dfree(dRec_);
+  dfree(dRecLb_);
+  dfree(dOneLen_);
+  dfree(dOneIdx_);
+  dfree(dLists_);
   if (hPin_) cudaFreeHost(hPin_);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
@@ -101,16 +101,22 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
   device = device_;
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  {  // stream-ordered allocations: keep freed blocks in the device pool for reuse
+    cudaMemPool_t mp;
+    CK(cudaDeviceGetDefaultMemPool(&mp, device));
+    uint64_t keep = UINT64_MAX;
+    CK(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   CK(cudaEventCreate(&ev0_));
   CK(cudaEventCreate(&ev1_));
   CK(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device));
   CK(cudaMallocHost(&hPin_, 4 * sizeof(int)));
-  CK(cudaMalloc(&dX_, sizeof(double) * (size_t)n * p));
-  CK(cudaMalloc(&dy_, sizeof(double) * (size_t)n));
+  CK(cudaMallocAsync(&dX_, sizeof(double) * (size_t)n * p, stream_));
+  CK(cudaMallocAsync(&dy_, sizeof(double) * (size_t)n, stream_));
   if (int rc_ = h2d(dX_, X, sizeof(double) * (size_t)n * p)) return rc_;
   if (int rc_ = h2d(dy_, y, sizeof(double) * (size_t)n)) return rc_;
-  CK(cudaMalloc(&dMa_, sizeof(int)));
-  CK(cudaMalloc(&dErr_, sizeof(int)));
+  CK(cudaMallocAsync(&dMa_, sizeof(int), stream_));
+  CK(cudaMallocAsync(&dErr_, sizeof(int), stream_));
   CK(gemm_set_attrs());
   n2_ = next_pow2(std::max(p, 2));
   colE_ = column_E(n2_);
@@ -148,11 +154,11 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
         if (nb >= 1) pass_grid_ = sms_;
       }
     }
-    CK(cudaMalloc(&dBar_, sizeof(unsigned)));
-    CK(cudaMalloc(&dPassOut_, 4 * sizeof(long long)));
+    CK(cudaMallocAsync(&dBar_, sizeof(unsigned), stream_));
+    CK(cudaMallocAsync(&dPassOut_, 4 * sizeof(long long), stream_));
     const char* penv = getenv("BNBG_PASS_PROF");
     if (penv && penv[0] == '1') {
-      CK(cudaMalloc(&dPassProf_, 32 * sizeof(unsigned long long)));
+      CK(cudaMallocAsync(&dPassProf_, 32 * sizeof(unsigned long long), stream_));
       CK(cudaMemsetAsync(dPassProf_, 0, 32 * sizeof(unsigned long long), stream_));
     }
   }
@@ -166,6 +172,10 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
     if (int rc = ensure(pre)) return rc;
     if (int rc = ensure_pool_batch(pre)) return rc;
     if (int rc = pool_reserve(4 * pre)) return rc;
+    // re-opt / upload scratch for a pass of `pre` supports
+    if (int rc = ensure_aux(sizeof(double) * ((size_t)p * pre + (size_t)8 * pre * std::max(k, 1)) +
+                            (size_t)(64 << 10)))
+      return rc;
   }
   CK(cudaStreamSynchronize(stream_));
   if (L_ > 0.0) {
@@ -180,55 +190,55 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
 int Engine::ensure(int m) {
   if (m <= mcap_) return 0;
   int cap = std::max(m, std::max(16, mcap_ * 2));
-  cudaFree(dB_);
-  cudaFree(dV_);
-  cudaFree(dG_);
-  cudaFree(dR_);
-  cudaFree(dPL_);
-  cudaFree(dPC_);
-  cudaFree(dT_);
-  cudaFree(dBest_);
-  cudaFree(dLast_);
-  cudaFree(dState_);
-  cudaFree(dFrozen_);
-  cudaFree(dKbar_);
-  cudaFree(dPf_);
-  cudaFree(dStatus_);
-  cudaFree(dIters_);
-  cudaFree(dAct_);
-  cudaFree(dSup_);
-  cudaFree(dLen_);
-  cudaFree(dJb_);
+  dfree(dB_);
+  dfree(dV_);
+  dfree(dG_);
+  dfree(dR_);
+  dfree(dPL_);
+  dfree(dPC_);
+  dfree(dT_);
+  dfree(dBest_);
+  dfree(dLast_);
+  dfree(dState_);
+  dfree(dFrozen_);
+  dfree(dKbar_);
+  dfree(dPf_);
+  dfree(dStatus_);
+  dfree(dIters_);
+  dfree(dAct_);
+  dfree(dSup_);
+  dfree(dLen_);
+  dfree(dJb_);
   const size_t pm = (size_t)p * cap;
-  CK(cudaMalloc(&dB_, sizeof(double) * pm));
-  CK(cudaMalloc(&dV_, sizeof(double) * pm));
-  CK(cudaMalloc(&dG_, sizeof(double) * pm * nsplit_max_));
-  CK(cudaMalloc(&dR_, sizeof(double) * (size_t)n * cap));
-  CK(cudaMalloc(&dPL_, sizeof(double) * (size_t)nrb_max_ * cap));
-  CK(cudaMalloc(&dPC_, sizeof(double) * (size_t)nrb_max_ * cap));
-  CK(cudaMalloc(&dT_, sizeof(double) * cap));
-  CK(cudaMalloc(&dBest_, sizeof(double) * cap));
-  CK(cudaMalloc(&dLast_, sizeof(double) * cap));
-  CK(cudaMalloc(&dState_, pm));
-  CK(cudaMalloc(&dFrozen_, cap));
-  CK(cudaMalloc(&dKbar_, sizeof(int) * cap));
-  CK(cudaMalloc(&dPf_, sizeof(int) * cap));
-  CK(cudaMalloc(&dStatus_, sizeof(int) * cap));
-  CK(cudaMalloc(&dIters_, sizeof(int) * cap));
-  CK(cudaMalloc(&dAct_, sizeof(int) * cap));
-  CK(cudaMalloc(&dSup_, sizeof(int) * (size_t)cap * std::max(k, 1)));
-  CK(cudaMalloc(&dLen_, sizeof(int) * cap));
-  CK(cudaMalloc(&dJb_, sizeof(int) * cap));
+  CK(cudaMallocAsync(&dB_, sizeof(double) * pm, stream_));
+  CK(cudaMallocAsync(&dV_, sizeof(double) * pm, stream_));
+  CK(cudaMallocAsync(&dG_, sizeof(double) * pm * nsplit_max_, stream_));
+  CK(cudaMallocAsync(&dR_, sizeof(double) * (size_t)n * cap, stream_));
+  CK(cudaMallocAsync(&dPL_, sizeof(double) * (size_t)nrb_max_ * cap, stream_));
+  CK(cudaMallocAsync(&dPC_, sizeof(double) * (size_t)nrb_max_ * cap, stream_));
+  CK(cudaMallocAsync(&dT_, sizeof(double) * cap, stream_));
+  CK(cudaMallocAsync(&dBest_, sizeof(double) * cap, stream_));
+  CK(cudaMallocAsync(&dLast_, sizeof(double) * cap, stream_));
+  CK(cudaMallocAsync(&dState_, pm, stream_));
+  CK(cudaMallocAsync(&dFrozen_, cap, stream_));
+  CK(cudaMallocAsync(&dKbar_, sizeof(int) * cap, stream_));
+  CK(cudaMallocAsync(&dPf_, sizeof(int) * cap, stream_));
+  CK(cudaMallocAsync(&dStatus_, sizeof(int) * cap, stream_));
+  CK(cudaMallocAsync(&dIters_, sizeof(int) * cap, stream_));
+  CK(cudaMallocAsync(&dAct_, sizeof(int) * cap, stream_));
+  CK(cudaMallocAsync(&dSup_, sizeof(int) * (size_t)cap * std::max(k, 1), stream_));
+  CK(cudaMallocAsync(&dLen_, sizeof(int) * cap, stream_));
+  CK(cudaMallocAsync(&dJb_, sizeof(int) * cap, stream_));
   mcap_ = cap;
   return 0;
 }
 
 int Engine::ensure_aux(size_t bytes) {
   if (bytes <= aux_bytes_) return 0;
-  cudaFree(dAux_);
+  dfree(dAux_);
   dAux_ = nullptr;
   size_t cap = std::max(bytes, aux_bytes_ * 2);
-  CK(cudaMalloc(&dAux_, cap));
+  CK(cudaMallocAsync(&dAux_, cap, stream_));
   aux_bytes_ = cap;
   return 0;
 }
@@ -645,7 +655,7 @@ int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_
   const int max_evals = cfg.max_iterations / std::max(1, cfg.check_interval) + 2;
   double* dTrace = nullptr;
   if (want_trace) {
-    CK(cudaMalloc(&dTrace, sizeof(double) * (size_t)max_evals * mcap_));
+    CK(cudaMallocAsync(&dTrace, sizeof(double) * (size_t)max_evals * mcap_, stream_));
     CK(cudaMemsetAsync(dTrace, 0xff, sizeof(double) * (size_t)max_evals * mcap_, stream_));
   }
   const int big = 0x7fffffff;
@@ -712,7 +722,7 @@ int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_
   CK(cudaStreamSynchronize(stream_));
   resolve_timing();
 done:
-  if (dTrace) cudaFree(dTrace);
+  if (dTrace) dfree(dTrace);
   return rc;
 }
 

@@ -122,6 +122,11 @@ class Engine {
 
  private:
   int ensure(int m);
+  // stream-ordered device allocations (cudaMallocAsync on the engine stream):
+  // freeing does not synchronise the device
+  void dfree(void* q) {
+    if (q) cudaFreeAsync(q, stream_);
+  }
   int pool_cap_ = 0;
   void* pool_mem_[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   int* dSlots_ = nullptr;    // batch slot ids (m)

@@ -43,11 +43,11 @@ int Engine::pool_reserve(int cap) {
                          sizeof(int) * (size_t)kk, sizeof(int), sizeof(int), sizeof(int)};
   for (int a = 0; a < 7; ++a) {
     void* nb = nullptr;
-    CK(cudaMalloc(&nb, per[a] * cap));
+    CK(cudaMallocAsync(&nb, per[a] * cap, stream_));
     if (pool_mem_[a]) {
       CK(cudaMemcpyAsync(nb, pool_mem_[a], per[a] * pool_cap_, cudaMemcpyDeviceToDevice, stream_));
       CK(cudaStreamSynchronize(stream_));
-      cudaFree(pool_mem_[a]);
+      dfree(pool_mem_[a]);
     }
     pool_mem_[a] = nb;
   }
@@ -67,28 +67,28 @@ int Engine::ensure_pool_batch(int m) {
   if (m <= pool_batch_cap_) return 0;
   const int cap = std::max(m, std::max(16, pool_batch_cap_ * 2));
   const int kk = std::max(k, 1);
-  cudaFree(dSlots_);
-  cudaFree(dLbIn_);
-  cudaFree(dLbOut_);
-  cudaFree(dPos_);
-  cudaFree(dTot_);
-  cudaFree(dFree_);
-  cudaFree(dRec_);
-  cudaFree(dRecLb_);
-  cudaFree(dOneLen_);
-  cudaFree(dOneIdx_);
-  cudaFree(dLists_);
+  dfree(dSlots_);
+  dfree(dLbIn_);
+  dfree(dLbOut_);
+  dfree(dPos_);
+  dfree(dTot_);
+  dfree(dFree_);
+  dfree(dRec_);
+  dfree(dRecLb_);
+  dfree(dOneLen_);
+  dfree(dOneIdx_);
+  dfree(dLists_);
   dLists_ = nullptr;
-  CK(cudaMalloc(&dSlots_, sizeof(int) * cap));
-  CK(cudaMalloc(&dLbIn_, sizeof(double) * cap));
-  CK(cudaMalloc(&dLbOut_, sizeof(double) * cap));
-  CK(cudaMalloc(&dPos_, sizeof(int) * cap));
-  CK(cudaMalloc(&dTot_, sizeof(int) * 2));
-  CK(cudaMalloc(&dFree_, sizeof(int) * 2 * (size_t)cap));
-  CK(cudaMalloc(&dRec_, sizeof(int) * 2 * (size_t)cap * child_rec_ints(kk)));
-  CK(cudaMalloc(&dRecLb_, sizeof(double) * 2 * (size_t)cap));
-  CK(cudaMalloc(&dOneLen_, sizeof(int) * cap));
-  CK(cudaMalloc(&dOneIdx_, sizeof(int) * (size_t)cap * kk));
+  CK(cudaMallocAsync(&dSlots_, sizeof(int) * cap, stream_));
+  CK(cudaMallocAsync(&dLbIn_, sizeof(double) * cap, stream_));
+  CK(cudaMallocAsync(&dLbOut_, sizeof(double) * cap, stream_));
+  CK(cudaMallocAsync(&dPos_, sizeof(int) * cap, stream_));
+  CK(cudaMallocAsync(&dTot_, sizeof(int) * 2, stream_));
+  CK(cudaMallocAsync(&dFree_, sizeof(int) * 2 * (size_t)cap, stream_));
+  CK(cudaMallocAsync(&dRec_, sizeof(int) * 2 * (size_t)cap * child_rec_ints(kk), stream_));
+  CK(cudaMallocAsync(&dRecLb_, sizeof(double) * 2 * (size_t)cap, stream_));
+  CK(cudaMallocAsync(&dOneLen_, sizeof(int) * cap, stream_));
+  CK(cudaMallocAsync(&dOneIdx_, sizeof(int) * (size_t)cap * kk, stream_));
   pool_batch_cap_ = cap;
   return 0;
 }
@@ -107,7 +107,7 @@ int Engine::relax_pool(int m, const int* slots, const RelaxParams& cfg, double t
   CKL("k_pack_pool");
   if (lists) {
     const size_t ints = (size_t)m * (2 + p + kk);
-    if (!dLists_) CK(cudaMalloc(&dLists_, sizeof(int) * (size_t)pool_batch_cap_ * (2 + p + kk)));
+    if (!dLists_) CK(cudaMallocAsync(&dLists_, sizeof(int) * (size_t)pool_batch_cap_ * (2 + p + kk), stream_));
     k_pool_lists<<<m, 128, 0, stream_>>>(P, m, dSlots_, dLists_, dLists_ + 2 * m,
                                          dLists_ + (size_t)m * (2 + p));
     CKL("k_pool_lists");
