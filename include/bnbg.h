@@ -203,7 +203,9 @@ typedef struct {
 } bnbg_comm_ops;
 
 /* NCCL bootstrap: rank 0 creates the id, the caller broadcasts its 128 bytes
- * (e.g. torch.distributed), then every rank binds its handle. */
+ * (e.g. torch.distributed), then every rank binds its handle.  Communicators
+ * are cached per process by (id, device, rank, world): binding a later handle
+ * with the same id reuses the communicator. */
 int bnbg_nccl_unique_id(uint8_t* uid_out /* 128 bytes */);
 int bnbg_nccl_init(bnbg_handle* h, const uint8_t* uid /* 128 bytes */, int rank, int world);
 

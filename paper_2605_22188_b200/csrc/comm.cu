@@ -4,6 +4,9 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
 #include <vector>
 
 #include "comm.hpp"
@@ -101,6 +104,16 @@ int Engine::pool_unpack(int cnt, const int* slots, double* lbs) {
   return 0;
 }
 
+// Process-wide communicator cache: an engine created later in the same process
+// (same device, rank, world and unique id) reuses the communicator instead of
+// paying ncclCommInitRank / ncclCommDestroy again.  Cached communicators live
+// until the process exits.
+static std::mutex g_comm_mu;
+static std::map<std::string, ncclComm_t>& comm_cache() {
+  static std::map<std::string, ncclComm_t> m;
+  return m;
+}
+
 void Engine::comm_release() {
   dfree(dXSend_);
   dfree(dXRecv_);
@@ -111,18 +124,23 @@ void Engine::comm_release() {
   dXSlots_ = nullptr;
   dXLb_ = nullptr;
   dGather_ = nullptr;
-  if (nccl_comm) ncclCommDestroy(static_cast<ncclComm_t>(nccl_comm));
-  nccl_comm = nullptr;
+  nccl_comm = nullptr;  // owned by the process-wide cache
 }
 
 int Engine::nccl_init(const uint8_t* uid, int rank, int world) {
   CK(cudaSetDevice(device));
-  ncclUniqueId id;
-  std::memcpy(&id, uid, sizeof(id));
-  ncclComm_t c = nullptr;
-  NK(ncclCommInitRank(&c, world, id, rank));
-  if (nccl_comm) ncclCommDestroy(static_cast<ncclComm_t>(nccl_comm));
-  nccl_comm = c;
+  std::string key(reinterpret_cast<const char*>(uid), sizeof(ncclUniqueId));
+  key += ":" + std::to_string(device) + ":" + std::to_string(rank) + ":" + std::to_string(world);
+  std::lock_guard<std::mutex> lk(g_comm_mu);
+  auto it = comm_cache().find(key);
+  if (it == comm_cache().end()) {
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof(id));
+    ncclComm_t c = nullptr;
+    NK(ncclCommInitRank(&c, world, id, rank));
+    it = comm_cache().emplace(key, c).first;
+  }
+  nccl_comm = it->second;
   nccl_rank = rank;
   nccl_world = world;
   return 0;

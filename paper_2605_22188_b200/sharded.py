@@ -73,19 +73,27 @@ class HostTransport:
             return 1
 
 
+_UIDS = {}  # (group, world) -> NCCL unique id shared by every engine of this process
+
+
 def nccl_bind(engine, group=None):
-    """Create the engine's NCCL communicator over the group's ranks."""
+    """Bind the engine to an NCCL communicator over the group's ranks.  The
+    unique id is drawn and broadcast once per group; later engines of the
+    process reuse the library's cached communicator (no re-initialisation)."""
     torch, dist = _torch_dist()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    uid = C.create_string_buffer(128)
-    if rank == 0:
-        if _L.lib().bnbg_nccl_unique_id(uid) != 0:
-            raise RuntimeError("bnbg_nccl_unique_id failed")
-    obj = [bytes(uid.raw) if rank == 0 else None]
-    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0,
-                               group=group)
+    key = (id(group), world)
+    if key not in _UIDS:
+        uid = C.create_string_buffer(128)
+        if rank == 0:
+            if _L.lib().bnbg_nccl_unique_id(uid) != 0:
+                raise RuntimeError("bnbg_nccl_unique_id failed")
+        obj = [bytes(uid.raw) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0,
+                                   group=group)
+        _UIDS[key] = obj[0]
     from . import _check
-    _check(_L.lib().bnbg_nccl_init(engine.handle, obj[0], rank, world), engine.handle)
+    _check(_L.lib().bnbg_nccl_init(engine.handle, _UIDS[key], rank, world), engine.handle)
 
 
 def solve_sharded(engine, config=None, group=None, transport: Optional[str] = None):
