@@ -153,6 +153,34 @@ int bnbg_select_branch(bnbg_handle* h, int m, const double* beta, const uint8_t*
 int bnbg_reoptimize(bnbg_handle* h, int nsup, const int32_t* offsets, const int32_t* idx,
                     double* coef_out, double* obj_out);
 
+/* ---- device-resident node pool: the per-pass successor of the seam ---------
+ * (SURVEY 8(b) item 4).  Open nodes live in the handle's HBM pool, one slot
+ * each (states, warm start, ordered J0/J1 lists); a caller keeping its own
+ * best-bound queue over (bound, sequence, slot) runs run_bnb's node-processing
+ * body (bnb_engine.hpp:179-256) with these calls, and no warm start or beta
+ * crosses PCIe.  bnbg_solve is exactly this loop. */
+
+/* root_node (node_model.hpp:47-52) into `slot` (the pool grows as needed) */
+int bnbg_pool_root(bnbg_handle* h, int slot);
+/* solve_batch_relaxation + round_support + select_branch_variable over the
+ * nodes in slots[m] (relaxation.hpp:163-255, primal_heuristics.hpp:134-163).
+ * Outputs: bounds (best dual), status, iterations per node; support_out m x k
+ * (J1 in fixing order ++ top-kbar free) with lengths len_out.  The betas stay
+ * on the device for bnbg_pool_branch. */
+int bnbg_pool_relax(bnbg_handle* h, const bnbg_relax_cfg* cfg, int m, const int32_t* slots,
+                    double prune_threshold, double* bounds_out, int32_t* status_out,
+                    int32_t* iters_out, int32_t* support_out, int32_t* len_out);
+/* The prune test and branch of the last bnbg_pool_relax batch
+ * (bnb_engine.hpp:242-256, node_model.hpp:57-105): node b survives iff its
+ * status is not prunable and max(lb_in[b], bound_b) < post_threshold; its two
+ * children (J0 + j, J1 + j) go to free_slots[2i], free_slots[2i+1] for the
+ * i-th survivor.  rec_out receives 2 x survivors records of (4 + k) ints:
+ * slot, leaf flag, |J1|, depth, J1 list; child_lb_out 2 x survivors bounds.
+ * Returns BNBG_LOGIC_ERROR when a survivor has no free coordinate. */
+int bnbg_pool_branch(bnbg_handle* h, int m, const double* lb_in, double post_threshold,
+                     const int32_t* free_slots, int32_t* survivors_out, int32_t* rec_out,
+                     double* child_lb_out);
+
 /* ---- stateless kernel entry points (prox_kernel.hpp) ---------------------- */
 /* prox_kernel.hpp:284-301 prox_step: out = U - rho^-1 prox_{rho g*}(rho U). */
 int bnbg_prox_step(int device, int p, int m, const double* U, double eta, double lambda2,

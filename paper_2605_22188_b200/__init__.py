@@ -508,6 +508,43 @@ class Engine:
         _check(_L.lib().bnbg_solve(self._h, C.byref(cfg), C.byref(cc), dh, bh, None), self._h)
         return _cert_from_c(cc, sup, coef)
 
+    # -- device-resident node pool, per pass (include/bnbg.h bnbg_pool_*) -------
+    def pool_root(self, slot: int = 0):
+        """root_node (node_model.hpp:47-52) into pool `slot`."""
+        _check(_L.lib().bnbg_pool_root(self._h, slot), self._h)
+
+    def pool_relax(self, slots, prune_threshold: float = math.inf,
+                   config: Optional[RelaxConfig] = None):
+        """Lower bounds + rounding + branch variable of the nodes in `slots`
+        (relaxation.hpp:163-255).  Returns (bounds, status, iterations,
+        supports) with supports in construction order (J1 ++ top-kbar free)."""
+        sl = np.ascontiguousarray(np.asarray(slots, dtype=np.int32))
+        m, k = len(sl), max(self.inst.k, 1)
+        cfg = (config or RelaxConfig()).to_c()
+        bd, st, it = np.zeros(m), np.zeros(m, np.int32), np.zeros(m, np.int32)
+        sup, ln = np.zeros(m * k, np.int32), np.zeros(m, np.int32)
+        _check(_L.lib().bnbg_pool_relax(self._h, C.byref(cfg), m, sl, prune_threshold, bd, st, it,
+                                        sup, ln), self._h)
+        rows = [sup[b * k: b * k + ln[b]].tolist() for b in range(m)]
+        return bd, st, it, rows
+
+    def pool_branch(self, lb, post_threshold: float, free_slots):
+        """Prune test + branch of the last pool_relax batch (bnb_engine.hpp:242-256).
+        Returns one (slot, is_leaf, fixed_one, depth, lower_bound) per child."""
+        lb = np.ascontiguousarray(np.asarray(lb, dtype=np.float64))
+        fs = np.ascontiguousarray(np.asarray(free_slots, dtype=np.int32))
+        m, k = len(lb), max(self.inst.k, 1)
+        rec = np.zeros(2 * m * (4 + k), np.int32)
+        clb = np.zeros(2 * m)
+        surv = C.c_int32()
+        _check(_L.lib().bnbg_pool_branch(self._h, m, lb, post_threshold, fs, C.byref(surv), rec,
+                                         clb), self._h)
+        out = []
+        for c in range(2 * surv.value):
+            r = rec[c * (4 + k):(c + 1) * (4 + k)]
+            out.append((int(r[0]), bool(r[1]), r[4:4 + r[2]].tolist(), int(r[3]), float(clb[c])))
+        return out
+
     # -- node-sharded solve over ranks (SURVEY 8(e); include/bnbg.h) ------------
     def solve_sharded(self, config: Optional[SolverConfig] = None, group=None,
                       transport: Optional[str] = None) -> Certificate:

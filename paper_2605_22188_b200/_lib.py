@@ -70,7 +70,7 @@ EXPORTS = [
     "bnbg_pool_size", "bnbg_pool_record", "bnbg_pool_free", "bnbg_kernel_launches",
     "bnbg_gemm_stats", "bnbg_set_timing", "bnbg_kernel_stats", "bnbg_transfer_bytes",
     "bnbg_pass_profile", "bnbg_nccl_unique_id", "bnbg_nccl_init", "bnbg_solve_sharded",
-    "bnbg_balance_plan",
+    "bnbg_balance_plan", "bnbg_pool_root", "bnbg_pool_relax", "bnbg_pool_branch",
 ]
 
 
@@ -124,6 +124,9 @@ def lib():
     L.bnbg_kernel_stats.argtypes = [vp, i, C.POINTER(d), C.POINTER(d), C.POINTER(ll)]
     L.bnbg_transfer_bytes.argtypes = [vp, C.POINTER(ll), C.POINTER(ll)]
     L.bnbg_pass_profile.argtypes = [vp, dp, i]
+    L.bnbg_pool_root.argtypes = [vp, i]
+    L.bnbg_pool_relax.argtypes = [vp, C.POINTER(RelaxCfgC), i, ip, d, dp, ip, ip, ip, ip]
+    L.bnbg_pool_branch.argtypes = [vp, i, dp, d, ip, C.POINTER(C.c_int32), ip, dp]
     L.bnbg_nccl_unique_id.argtypes = [C.c_char_p]
     L.bnbg_nccl_init.argtypes = [vp, C.c_char_p, i, i]
     L.bnbg_solve_sharded.argtypes = [vp, C.POINTER(SolverCfgC), C.POINTER(CommOpsC),

@@ -26,6 +26,8 @@
 
 struct bnbg_handle {
   bnbg::Engine eng;
+  int last_pool_m = 0;                 // batch of the last bnbg_pool_relax
+  std::vector<int> last_pool_slots;
 };
 
 struct bnbg_pool {
@@ -702,6 +704,69 @@ int bnbg_reoptimize(bnbg_handle* h, int nsup, const int32_t* offsets, const int3
         return set_err(h, BNBG_INPUT_ERROR, "reoptimize_supports: index out of range");
   const int rc = h->eng.reoptimize(nsup, offsets, idx, coef_out, obj_out);
   return rc ? set_err(h, rc, h->eng.err) : BNBG_OK;
+}
+
+int bnbg_pool_root(bnbg_handle* h, int slot) {
+  if (slot < 0) return set_err(h, BNBG_INPUT_ERROR, "pool_root: slot must be nonnegative");
+  const int rc = h->eng.pool_root(slot);
+  return rc ? set_err(h, rc, h->eng.err) : BNBG_OK;
+}
+
+int bnbg_pool_relax(bnbg_handle* h, const bnbg_relax_cfg* cfg, int m, const int32_t* slots,
+                    double prune_threshold, double* bounds_out, int32_t* status_out,
+                    int32_t* iters_out, int32_t* support_out, int32_t* len_out) {
+  bnbg_relax_cfg c;
+  if (cfg)
+    c = *cfg;
+  else
+    bnbg_relax_cfg_default(&c);
+  if (m <= 0) return set_err(h, BNBG_INPUT_ERROR, "solve_batch_relaxation: empty batch");
+  if (c.check_interval < 1 || c.max_iterations < 1)
+    return set_err(h, BNBG_INPUT_ERROR, "relax config: max_iterations, check_interval >= 1");
+  for (int b = 0; b < m; ++b)
+    if (slots[b] < 0 || slots[b] >= h->eng.pool_capacity())
+      return set_err(h, BNBG_INPUT_ERROR, "pool_relax: slot out of range");
+  const double saved_L = h->eng.L;
+  if (c.smoothness > 0.0) h->eng.L = c.smoothness;
+  bnbg::PassResult pr;
+  const int rc =
+      h->eng.relax_pool(m, slots, relax_params(c), prune_threshold, false, pr, false, nullptr,
+                        nullptr, nullptr);
+  h->eng.L = saved_L;
+  if (rc) return set_err(h, rc, h->eng.err);
+  const int kk = std::max(h->eng.k, 1);
+  std::memcpy(bounds_out, pr.bounds.data(), sizeof(double) * m);
+  std::memcpy(status_out, pr.status.data(), sizeof(int) * m);
+  std::memcpy(iters_out, pr.iters.data(), sizeof(int) * m);
+  if (support_out) std::memcpy(support_out, pr.sup.data(), sizeof(int) * (size_t)m * kk);
+  if (len_out) std::memcpy(len_out, pr.len.data(), sizeof(int) * m);
+  h->last_pool_m = m;
+  h->last_pool_slots.assign(slots, slots + m);
+  return BNBG_OK;
+}
+
+int bnbg_pool_branch(bnbg_handle* h, int m, const double* lb_in, double post_threshold,
+                     const int32_t* free_slots, int32_t* survivors_out, int32_t* rec_out,
+                     double* child_lb_out) {
+  if (m != h->last_pool_m || m <= 0)
+    return set_err(h, BNBG_INPUT_ERROR, "pool_branch: m must match the last pool_relax batch");
+  for (int i = 0; i < 2 * m; ++i)
+    if (free_slots[i] < 0)
+      return set_err(h, BNBG_INPUT_ERROR, "pool_branch: free slots must be nonnegative");
+  int hw = 0;
+  for (int i = 0; i < 2 * m; ++i) hw = std::max(hw, free_slots[i] + 1);
+  if (int rc = h->eng.pool_reserve(hw)) return set_err(h, rc, h->eng.err);
+  int surv = 0, bad = -1;
+  std::vector<int> rec;
+  std::vector<double> rlb;
+  const int rc = h->eng.branch_pool(m, h->last_pool_slots.data(), lb_in, post_threshold,
+                                    free_slots, surv, bad, rec, rlb);
+  if (rc) return set_err(h, rc, h->eng.err);
+  if (bad >= 0) return set_err(h, BNBG_LOGIC_ERROR, "select_branch_variable: no free coordinate");
+  *survivors_out = surv;
+  if (rec_out && !rec.empty()) std::memcpy(rec_out, rec.data(), sizeof(int) * rec.size());
+  if (child_lb_out && !rlb.empty()) std::memcpy(child_lb_out, rlb.data(), sizeof(double) * rlb.size());
+  return BNBG_OK;
 }
 
 int bnbg_gemm(bnbg_handle* h, int trans, int m, const double* B, double* C) {
