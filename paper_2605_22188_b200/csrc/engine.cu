@@ -830,9 +830,24 @@ int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coe
       rpt = need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : 8;
     }
   }
-  const bool direct = !gram && !cs && qmax <= 16;
+  // large n: X_S slices in shared memory, 8 or 16 CTAs per support
+  // (BNBG_REOPT_SMEM=0 falls back to the per-CTA gather form)
+  int cs_smem = 0;
+  static const bool smem_ok = [] {
+    const char* e = getenv("BNBG_REOPT_SMEM");
+    return !(e && e[0] == '0');
+  }();
+  if (smem_ok && !gram && !cs && qmax <= 16) {
+    for (int c : {8, 16}) {
+      if (reopt_smem_bytes(n, qmax, c) <= 200 * 1024) {
+        cs_smem = c;
+        break;
+      }
+    }
+  }
+  const bool direct = !gram && !cs && !cs_smem && qmax <= 16;
   // the deriv scratch is only used by the generic kernel
-  const size_t scr = (gram || direct || cs) ? 0 : (size_t)nsup * n;
+  const size_t scr = (gram || direct || cs || cs_smem) ? 0 : (size_t)nsup * n;
   const size_t bytes = sizeof(double) * (scr + tot + nsup + 2) +
                        sizeof(int) * ((size_t)2 * nsup + 1 + tot + 2);
   if (int rc = ensure_aux(bytes)) return rc;
@@ -854,6 +869,10 @@ int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coe
     ++launches;
     CK(launch_reopt_cluster(qmax <= 8 ? 8 : 16, rpt, cs, nsup, stream_, n, dX_, dy_, loss, M,
                             lambda2, step, d_off, d_idx, d_coef, d_obj, d_its));
+  } else if (cs_smem) {
+    ++launches;
+    CK(launch_reopt_smem(qmax, cs_smem, nsup, stream_, n, dX_, dy_, loss, M, lambda2, step, d_off,
+                         d_idx, d_coef, d_obj, d_its));
   } else if (qmax <= 8) {
     k_reopt_direct<8><<<nsup, kReoptFastThreads, 0, stream_>>>(
         n, dX_, dy_, loss, M, lambda2, step, d_off, d_idx, d_scr, d_coef, d_obj, d_its);

@@ -78,6 +78,12 @@ cudaError_t launch_reopt_cluster(int qmax, int rpt, int cs, int nsup, cudaStream
                                  double lambda2, double step, const int* off, const int* idx,
                                  double* coef, double* obj, int* its);
 
+// large-n variant: X_S slice in shared memory, cs <= 16 CTAs per support
+size_t reopt_smem_bytes(int n, int qmax, int cs);
+cudaError_t launch_reopt_smem(int qmax, int cs, int nsup, cudaStream_t st, int n, const double* X,
+                              const double* y, int loss, double M, double lambda2, double step,
+                              const int* off, const int* idx, double* coef, double* obj, int* its);
+
 // ---- pass_kernels.cu -------------------------------------------------------
 size_t pass_smem(int p, int n2, int E);
 // residency plan for `grid` CTAs (res.on = 0 when X does not fit); returns the

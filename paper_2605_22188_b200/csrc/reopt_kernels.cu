@@ -47,4 +47,48 @@ cudaError_t launch_reopt_cluster(int qmax, int rpt, int cs, int nsup, cudaStream
   return cudaErrorInvalidValue;
 }
 
+size_t reopt_smem_bytes(int n, int qmax, int cs) {
+  const int qm = qmax <= 8 ? 8 : 16;
+  const size_t rows = (size_t)(n + cs - 1) / cs;
+  return sizeof(double) * (rows * qm + rows);
+}
+
+template <int Q>
+static cudaError_t launch_smem_q(int cs, int nsup, cudaStream_t st, int n, const double* X,
+                                 const double* y, int loss, double M, double lambda2, double step,
+                                 const int* off, const int* idx, double* coef, double* obj,
+                                 int* its) {
+  const size_t smem = reopt_smem_bytes(n, Q, cs);
+  cudaError_t e = cudaFuncSetAttribute(k_reopt_cluster_smem<Q>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess && cs > 8)
+    e = cudaFuncSetAttribute(k_reopt_cluster_smem<Q>,
+                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nsup * cs);
+  cfg.blockDim = dim3(kReoptSmemThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_reopt_cluster_smem<Q>, n, X, y, loss, M, lambda2, step, off,
+                            idx, coef, obj, its);
+}
+
+cudaError_t launch_reopt_smem(int qmax, int cs, int nsup, cudaStream_t st, int n, const double* X,
+                              const double* y, int loss, double M, double lambda2, double step,
+                              const int* off, const int* idx, double* coef, double* obj,
+                              int* its) {
+  if (qmax <= 8)
+    return launch_smem_q<8>(cs, nsup, st, n, X, y, loss, M, lambda2, step, off, idx, coef, obj,
+                            its);
+  return launch_smem_q<16>(cs, nsup, st, n, X, y, loss, M, lambda2, step, off, idx, coef, obj, its);
+}
+
 }  // namespace bnbg

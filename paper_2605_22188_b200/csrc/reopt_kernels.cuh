@@ -508,6 +508,140 @@ __global__ void __launch_bounds__(kReoptClusterThreads)
   }
 }
 
+// k_reopt_cluster_smem: the large-n variant (c4: n = 20000, where X_S no
+// longer fits 8 CTAs' registers).  Each CTA keeps its X_S slice and y in
+// shared memory, column-major so consecutive threads read consecutive rows
+// (conflict-free), with up to 16 CTAs per support (non-portable cluster
+// size); the exchange is k_reopt_cluster_mb's st.async + mbarrier scheme.
+constexpr int kReoptSmemThreads = 256;
+constexpr int kReoptSmemMaxCluster = 16;
+
+template <int QMAX>
+__global__ void __launch_bounds__(kReoptSmemThreads)
+    k_reopt_cluster_smem(int n, const double* __restrict__ X, const double* __restrict__ y,
+                         int loss, double M, double lambda2, double step, const int* off,
+                         const int* sidx, double* coef_out, double* obj_out, int* it_out) {
+  namespace cg = cooperative_groups;
+  constexpr int NT = kReoptSmemThreads, NW = NT / 32;
+  extern __shared__ __align__(16) double xsl[];  // QMAX columns of `chunk` rows, then y
+  cg::cluster_group cl = cg::this_cluster();
+  const int CS = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  const int s = blockIdx.x / CS;
+  __shared__ double red[2][NW][QMAX];
+  __shared__ __align__(16) double xsum[2][kReoptSmemMaxCluster][QMAX];
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ double fin[kReoptSmemMaxCluster];
+  __shared__ double wred[NW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = off[s + 1] - off[s];
+  const int* S = sidx + off[s];
+  const int chunk = (n + CS - 1) / CS;
+  const int r0 = rank * chunk, r1 = min(n, r0 + chunk), rows = max(0, r1 - r0);
+  double* ysl = xsl + (size_t)chunk * QMAX;
+  const uint32_t bytes = (uint32_t)(CS * QMAX * sizeof(double));
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    mbar_arm(&mbar[0], bytes);
+    mbar_arm(&mbar[1], bytes);
+  }
+  for (int r = 0; r < QMAX; ++r)
+    for (int i = tid; i < rows; i += NT)
+      xsl[(size_t)r * chunk + i] = r < q ? X[(size_t)S[r] * n + r0 + i] : 0.0;
+  for (int i = tid; i < rows; i += NT) ysl[i] = y[r0 + i];
+  cl.sync();
+  uint32_t dst_slot = 0, dst_bar = 0;
+  const int my_dst = tid / QMAX, my_r = tid % QMAX;
+  if (tid < CS * QMAX) {
+    dst_slot = cluster_map(smem_addr(&xsum[0][rank][my_r]), (uint32_t)my_dst);
+    dst_bar = cluster_map(smem_addr(&mbar[0]), (uint32_t)my_dst);
+  }
+  const uint32_t buf_stride = (uint32_t)(kReoptSmemMaxCluster * QMAX * sizeof(double));
+  double beta[QMAX];
+#pragma unroll
+  for (int r = 0; r < QMAX; ++r) beta[r] = 0.0;
+  const int ridx = reduce_scatter_index<QMAX>(lane);
+  const bool writer = (lane & (32 / QMAX - 1)) == 0;
+  int its = 0;
+  if (q > 0) {
+    for (int it = 0; it < 5000; ++it) {
+      ++its;
+      const int buf = it & 1;
+      double part[QMAX];
+#pragma unroll
+      for (int r = 0; r < QMAX; ++r) part[r] = 0.0;
+      for (int i = tid; i < rows; i += NT) {
+        double xv[QMAX];
+#pragma unroll
+        for (int r = 0; r < QMAX; ++r) xv[r] = xsl[(size_t)r * chunk + i];
+        double sc = 0.0;  // scores, r ascending (primal_heuristics.hpp:194-198)
+#pragma unroll
+        for (int r = 0; r < QMAX; ++r) sc += beta[r] * xv[r];
+        const double di = d_loss_deriv(loss, sc, ysl[i]);
+#pragma unroll
+        for (int r = 0; r < QMAX; ++r) part[r] += xv[r] * di;
+      }
+      warp_reduce_scatter<QMAX>(part, lane);
+      if (writer) red[buf][warp][ridx] = part[0];
+      __syncthreads();
+      if (tid == 0 && it > 0) mbar_arm(&mbar[buf ^ 1], bytes);
+      if (tid < CS * QMAX) {
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) v += red[buf][w][my_r];
+        st_async_f64(dst_slot + buf * buf_stride, v, dst_bar + buf * (uint32_t)sizeof(uint64_t));
+      }
+      mbar_wait(&mbar[buf], (uint32_t)((it >> 1) & 1));
+      double gs[QMAX];
+#pragma unroll
+      for (int r = 0; r < QMAX; ++r) gs[r] = 0.0;
+      for (int c = 0; c < CS; ++c) {
+        const double2* row = reinterpret_cast<const double2*>(xsum[buf][c]);
+#pragma unroll
+        for (int r2 = 0; r2 < QMAX / 2; ++r2) {
+          const double2 t = row[r2];
+          gs[2 * r2] += t.x;
+          gs[2 * r2 + 1] += t.y;
+        }
+      }
+      double gm2 = 0.0;
+#pragma unroll
+      for (int r = 0; r < QMAX; ++r) {
+        double g = gs[r] + 2.0 * lambda2 * beta[r];  // (:210-211)
+        double v = beta[r] - step * g;
+        v = v < -M ? -M : v;
+        v = v > M ? M : v;
+        const double dl = beta[r] - v;
+        gm2 += dl * dl;
+        beta[r] = r < q ? v : 0.0;
+      }
+      if (sqrt(gm2) / step <= 1e-8) break;  // (:212-215)
+    }
+  }
+  double acc = 0.0;  // objective (:217-222)
+  for (int i = tid; i < rows; i += NT) {
+    double sc = 0.0;
+#pragma unroll
+    for (int r = 0; r < QMAX; ++r) sc += beta[r] * xsl[(size_t)r * chunk + i];
+    acc += d_loss_value(loss, sc, ysl[i]);
+  }
+  const double cta = block_sum<NT>(acc, wred);
+  if (tid == 0) *cl.map_shared_rank(&fin[rank], 0) = cta;
+  cl.sync();
+  if (rank == 0 && tid == 0) {
+    double sq = 0.0;
+#pragma unroll
+    for (int r = 0; r < QMAX; ++r) sq += beta[r] * beta[r];
+    double obj = lambda2 * sq;
+    for (int c = 0; c < CS; ++c) obj += fin[c];
+    obj_out[s] = obj;
+    if (it_out) it_out[s] = its;
+    for (int r = 0; r < q && r < QMAX; ++r) coef_out[off[s] + r] = beta[r];
+  }
+}
+
 // k_reopt_gram (squared loss): X_S'(X_S beta - y) = Gram beta - X_S'y, the
 // same iterates in exact arithmetic.  The q x q Gram and
 // X_S'y are built once per support; warp 0 then runs the projected-gradient
