@@ -4,6 +4,7 @@ validation, auto batch size) agree with the oracle.  No device calls."""
 import ctypes as C
 import os
 import re
+import subprocess
 
 import numpy as np
 import pytest
@@ -80,3 +81,19 @@ def test_product_does_not_import_oracle():
                 text = open(os.path.join(dirpath, fn)).read()
                 assert "import oracle" not in text and "from oracle" not in text
                 assert "oracle.h" not in text and "liboracle" not in text
+
+
+def _build_c_client(tmp_path):
+    exe = tmp_path / "solve_c"
+    cmd = ["gcc", "-std=c99", "-Wall", "-Werror", "-O2", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "examples", "solve_c.c"), "-L",
+           os.path.join(ROOT, "paper_2605_22188_b200"), "-lbnbg",
+           "-Wl,-rpath," + os.path.join(ROOT, "paper_2605_22188_b200"), "-o", str(exe)]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/bnbg.h compiles as C99 and a C client links against libbnbg.so
+    (the C-ABI boundary: no C++ types, no exceptions)."""
+    assert _build_c_client(tmp_path).exists()

@@ -144,3 +144,19 @@ def test_zero_response_and_time_limit(bnb):
     big = _inst(bnb, 300, 80, 8, 0.9, 0, 1)
     c = bnb.solve(big, bnb.SolverConfig(time_limit=0.0))
     assert c.status == "time_limit" and c.gap_percent == 100.0
+
+
+def test_c_client_certifies_like_python(bnb, tmp_path):
+    """The plain-C client (examples/solve_c.c) through the C-ABI gives the same
+    certificate as the Python mirror."""
+    import json
+    import subprocess
+    from tests.test_boundary_cpu import _build_c_client
+    exe = _build_c_client(tmp_path)
+    out = subprocess.run([str(exe), "300", "60", "5", "0.8", "1", "3"], capture_output=True,
+                         text=True, check=True).stdout
+    got = json.loads(out.strip().splitlines()[-1])
+    inst = _inst(bnb, 300, 60, 5, 0.8, 1, 3)
+    ref = bnb.solve(inst)
+    assert got["support"] == ref.support and got["status"] == 0
+    assert got["optimal_value"] == ref.optimal_value and got["nodes"] == ref.nodes_processed
