@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbnbg.so")
+# BNBG_LIB_PATH: load another build of the library (kernel-variant experiments)
+LIB_PATH = os.environ.get("BNBG_LIB_PATH") or os.path.join(_HERE, "libbnbg.so")
 _lib = None
 
 

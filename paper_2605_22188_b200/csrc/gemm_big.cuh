@@ -16,7 +16,13 @@
 namespace bnbg {
 
 constexpr int kBigThreads = 256;
-constexpr int kBigBM = 128, kBigBN = 64, kBigBK = 16, kBigNS = 3;
+#ifndef BNBG_BIG_BK
+#define BNBG_BIG_BK 16
+#endif
+#ifndef BNBG_BIG_NS
+#define BNBG_BIG_NS 3
+#endif
+constexpr int kBigBM = 128, kBigBN = 64, kBigBK = BNBG_BIG_BK, kBigNS = BNBG_BIG_NS;
 constexpr int kBigLDA_NN = kBigBM + 4;  // NN A tile stored [k][m]
 constexpr int kBigLDK = kBigBK + 4;     // [m][k] / [n][k] tiles
 constexpr int kBigA = kBigBK * kBigLDA_NN > kBigBM * kBigLDK ? kBigBK * kBigLDA_NN : kBigBM * kBigLDK;
@@ -46,27 +52,29 @@ __device__ void gemm_big_tile(const GemmArgs& g, int ncols, int mt, int nt, doub
     double* As = smem + stage * kBigStage;
     double* Bs = As + kBigA;
     const int k0 = kt * kBigBK;
-    // A: 128 x 16 doubles = 1024 16-byte chunks
+    // A: 128 x BK doubles in 16-byte chunks
+    constexpr int KC = kBigBK / 2;  // chunks per k-row (TN) ...
+    constexpr int MC = kBigBM / 2;  // ... and per m-row (NN)
 #pragma unroll
-    for (int it = 0; it < 4; ++it) {
+    for (int it = 0; it < kBigBM * kBigBK / 2 / kBigThreads; ++it) {
       const int e = tid + it * kBigThreads;
       if (TN) {  // A(m, k) = X[(m0+m)*n + k0 + k], contiguous in k; stored [m][k]
-        const int m = e >> 3, kc = (e & 7) * 2;
+        const int m = e / KC, kc = (e % KC) * 2;
         const int gm = m0 + m, gk = k0 + kc;
         const bool ok = gm < g.M && gk < K;
         cp_async_16(As + m * kBigLDK + kc, ok ? g.A + (size_t)gm * g.lda + gk : g.A, ok ? 16 : 0);
       } else {   // A(m, k) = X[(k0+k)*n + m0 + m], contiguous in m; stored [k][m]
-        const int k = e >> 6, mc = (e & 63) * 2;
+        const int k = e / MC, mc = (e % MC) * 2;
         const int gm = m0 + mc, gk = k0 + k;
         const bool ok = gm < g.M && gk < K;
         cp_async_16(As + k * kBigLDA_NN + mc, ok ? g.A + (size_t)gk * g.lda + gm : g.A, ok ? 16 : 0);
       }
     }
-    // B: 64 columns x 16 k = 512 chunks
+    // B: 64 columns x BK
 #pragma unroll
-    for (int it = 0; it < 2; ++it) {
+    for (int it = 0; it < kBigBN * kBigBK / 2 / kBigThreads; ++it) {
       const int e = tid + it * kBigThreads;
-      const int c = e >> 3, kc = (e & 7) * 2;
+      const int c = e / KC, kc = (e % KC) * 2;
       const int col = colmap[c];
       const int gk = k0 + kc;
       const bool ok = col >= 0 && gk < K;

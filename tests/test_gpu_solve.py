@@ -160,3 +160,18 @@ def test_c_client_certifies_like_python(bnb, tmp_path):
     ref = bnb.solve(inst)
     assert got["support"] == ref.support and got["status"] == 0
     assert got["optimal_value"] == ref.optimal_value and got["nodes"] == ref.nodes_processed
+
+
+def test_config_c5_rashomon_matches_oracle(bnb):
+    """BASELINE c5 (Rashomon set, epsilon 0.01, squared n=2000 p=500 k=8) vs the
+    oracle's pool (tests/golden/rashomon_c5.json, make_golden_c5.py)."""
+    ref = _load("rashomon_c5.json")
+    inst = _inst(bnb, 2000, 500, 8, 0.7, 0, 0)
+    res = bnb.collect_rashomon(inst, rconfig=bnb.RashomonConfig(epsilon=ref["epsilon"]))
+    cert = res.certificate
+    assert cert.support == ref["support"]
+    assert abs(cert.optimal_value - ref["optimal_value"]) <= REL * abs(ref["optimal_value"])
+    assert cert.nodes_processed == ref["nodes"]
+    assert [s for s, _, _ in res.pool] == [m["sequence"] for m in ref["pool"]]
+    np.testing.assert_allclose([o for _, _, o in res.pool], [m["objective"] for m in ref["pool"]],
+                               rtol=REL)
