@@ -810,7 +810,9 @@ int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coe
   if (!gram && qmax <= 16) {
     const int qm = qmax <= 8 ? 8 : 16;
     const int rpt_max = 64 / qm;
-    for (int c = 1; c <= kReoptMaxCluster; c <<= 1) {
+    // every (destination, value) pair of the exchange needs its own thread
+    const int cs_cap = std::min(kReoptMaxCluster, kReoptClusterThreads / qm);
+    for (int c = 1; c <= cs_cap; c <<= 1) {
       const int rows = (n + c - 1) / c;
       const int need = (rows + kReoptClusterThreads - 1) / kReoptClusterThreads;
       if (need <= rpt_max) {
@@ -821,9 +823,9 @@ int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coe
     if (cs) {
       const char* env = getenv("BNBG_REOPT_CS");
       if (env && atoi(env) > 0) {
-        cs = std::max(cs, std::min(kReoptMaxCluster, atoi(env)));
+        cs = std::max(cs, std::min(cs_cap, atoi(env)));
       } else {
-        while (cs < kReoptMaxCluster && nsup * cs * 2 <= sms_) cs <<= 1;
+        while (cs < cs_cap && nsup * cs * 2 <= sms_) cs <<= 1;
       }
       const int rows = (n + cs - 1) / cs;
       const int need = (rows + kReoptClusterThreads - 1) / kReoptClusterThreads;
@@ -867,8 +869,18 @@ int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coe
     CKL("k_reopt_gram");
   } else if (cs) {
     ++launches;
-    CK(launch_reopt_cluster(qmax <= 8 ? 8 : 16, rpt, cs, nsup, stream_, n, dX_, dy_, loss, M,
-                            lambda2, step, d_off, d_idx, d_coef, d_obj, d_its));
+    cudaError_t le = launch_reopt_cluster(qmax <= 8 ? 8 : 16, rpt, cs, nsup, stream_, n, dX_, dy_,
+                                          loss, M, lambda2, step, d_off, d_idx, d_coef, d_obj, d_its);
+    if (le != cudaSuccess && cs > 8) {  // 16-CTA clusters not schedulable here: portable size
+      (void)cudaGetLastError();
+      cs = 8;
+      const int rows = (n + cs - 1) / cs;
+      const int need = (rows + kReoptClusterThreads - 1) / kReoptClusterThreads;
+      rpt = need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : 8;
+      le = launch_reopt_cluster(qmax <= 8 ? 8 : 16, rpt, cs, nsup, stream_, n, dX_, dy_, loss, M,
+                                lambda2, step, d_off, d_idx, d_coef, d_obj, d_its);
+    }
+    CK(le);
   } else if (cs_smem) {
     ++launches;
     CK(launch_reopt_smem(qmax, cs_smem, nsup, stream_, n, dX_, dy_, loss, M, lambda2, step, d_off,

@@ -27,6 +27,12 @@ static cudaError_t launch_q_r(int cs, int nsup, cudaStream_t st, int n, const do
     const char* e = getenv("BNBG_REOPT_MB");  // 0: cluster-barrier exchange
     return !(e && e[0] == '0');
   }();
+  if (cs > 8) {
+    cudaError_t e = cudaFuncSetAttribute(mb ? (const void*)k_reopt_cluster_mb<Q, R>
+                                            : (const void*)k_reopt_cluster<Q, R>,
+                                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
   if (mb)
     return cudaLaunchKernelEx(&cfg, k_reopt_cluster_mb<Q, R>, n, X, y, loss, M, lambda2, step, off,
                               idx, coef, obj, its);
@@ -38,6 +44,9 @@ cudaError_t launch_reopt_cluster(int qmax, int rpt, int cs, int nsup, cudaStream
                                  const double* X, const double* y, int loss, double M,
                                  double lambda2, double step, const int* off, const int* idx,
                                  double* coef, double* obj, int* its) {
+  // the exchange maps one thread to each (destination, value) pair
+  if (cs < 1 || cs > kReoptMaxCluster || cs * qmax > kReoptClusterThreads)
+    return cudaErrorInvalidValue;
 #define RQ(Q, R)                                                                              \
   if (qmax == Q && rpt == R)                                                                  \
     return launch_q_r<Q, R>(cs, nsup, st, n, X, y, loss, M, lambda2, step, off, idx, coef, obj, \

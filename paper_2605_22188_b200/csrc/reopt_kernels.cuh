@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kReoptFastThreads)
 // per iteration, which makes one cluster barrier per iteration sufficient.
 // --------------------------------------------------------------------------
 constexpr int kReoptClusterThreads = 128;
-constexpr int kReoptMaxCluster = 8;
+constexpr int kReoptMaxCluster = 16;  // > 8 needs the non-portable cluster size
 
 // Warp reduce-scatter of QMAX partial sums (QMAX in {8, 16}): log2(QMAX)
 // halving exchanges, then a butterfly over the remaining lane bits -- 9
