@@ -67,7 +67,7 @@ struct ColProbe {
     if (!p) return;
     unsigned long long now;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    p[i] += now - t;
+    atomicAdd(p + i, now - t);  // RED: no load on the timed thread's path
     t = now;
   }
 };

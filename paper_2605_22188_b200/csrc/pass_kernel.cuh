@@ -425,12 +425,12 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
   auto mark = [&](int ph) {  // phase end (after its grid barrier)
     if (prof) {
       const unsigned long long t = pass_clock();
-      a.prof[ph] += t - t_last;
+      atomicAdd(a.prof + ph, t - t_last);  // RED: no load on CTA 0's path
       t_last = t;
     }
   };
   auto arrive = [&](int ph) {  // CTA 0 reaches the phase's barrier
-    if (prof) a.prof[8 + ph] += pass_clock() - t_last;
+    if (prof) atomicAdd(a.prof + 8 + ph, pass_clock() - t_last);
   };
   auto phase_nn = [&](const double* src, bool eval) {
     if (res) {
