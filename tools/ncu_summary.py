@@ -29,10 +29,14 @@ METRICS = {
     "launch__shared_mem_per_block_dynamic": "dyn_smem",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
     "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active": "dmma_pipe_pct",
+    "dram__bytes.sum.per_second": "dram_bytes_per_s",
+    "lts__t_bytes.sum.per_second": "l2_bytes_per_s",
+    "l1tex__t_bytes.sum.per_second": "l1_bytes_per_s",
     "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed":
         "tensor_pipe_elapsed_pct",
 }
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Kbyte/block": 1e3,
+SCALE = {"byte/second": 1, "Kbyte/second": 1e3, "Mbyte/second": 1e6, "Gbyte/second": 1e9,
+         "Tbyte/second": 1e12, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Kbyte/block": 1e3,
          "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0, "nsecond": 1e-9, "usecond": 1e-6,
          "msecond": 1e-3, "second": 1.0}
 
@@ -53,6 +57,8 @@ def summarise(path):
             continue
         d[key] = v * SCALE.get(units[i], 1.0)
     d["dram_bytes_per_launch"] = d.get("dram_read", 0.0) + d.get("dram_write", 0.0)
+    if d.get("duration_s"):
+        d["dram_gbs"] = d["dram_bytes_per_launch"] / d["duration_s"] / 1e9
     return d
 
 
