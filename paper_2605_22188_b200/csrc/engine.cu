@@ -163,6 +163,14 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
     }
   }
   nrb_max_ = (n + 15) / 16;
+  {  // per-iteration work above which streaming batches use the standalone kernels
+    const char* e = getenv("BNBG_PERSIST_MAXFLOPS");
+    persist_max_flops_ = e ? atof(e) : 4e9;
+  }
+  {  // active width from which the 128 x 64 GEMM tiles are used (BNBG_BIGGEMM=0: never)
+    const char* e = getenv("BNBG_BIGGEMM");
+    big_min_ = e ? std::max(0, atoi(e)) : 64;
+  }
   // batch workspaces and the node pool sized for a typical narrow frontier up
   // front, so the first passes of a solve do not pay cudaMalloc/cudaFree
   // (cudaFree synchronises the device) while the batch width grows
@@ -301,11 +309,7 @@ int Engine::d2h(void* dst, const void* src, size_t bytes) {
 Engine::GemmPlan Engine::plan(int Mr, int K, int ncols, bool allow_split) const {
   GemmPlan pl;
   // wide batches: register-tiled 128 x 64 tiles, no split-K (BNBG_BIGGEMM=0 disables)
-  static const bool big_ok = [] {
-    const char* e = getenv("BNBG_BIGGEMM");
-    return !(e && e[0] == '0');
-  }();
-  if (big_ok && ncols >= 64 && (n % 2) == 0 && (p % 2) == 0) {
+  if (big_min_ > 0 && ncols >= big_min_ && (n % 2) == 0 && (p % 2) == 0) {
     const int bm = gemm_big_tile_m(), bn = gemm_big_tile_n();
     pl.big = true;
     pl.fm = pl.fn = 0;
@@ -618,13 +622,7 @@ int Engine::run_pass(int m, const RelaxParams& cfg, double thr, double eta, doub
   a.tn.probe = dPassProf_ ? dPassProf_ + 24 : nullptr;
   a.bar = dBar_;
   a.res = res_;
-  {
-    static const bool big_ok = [] {
-      const char* e = getenv("BNBG_BIGGEMM");
-      return !(e && e[0] == '0');
-    }();
-    a.big = big_ok && (n % 2) == 0 && (p % 2) == 0;
-  }
+  a.big = ((n % 2) == 0 && (p % 2) == 0) ? big_min_ : 0;
   CK(cudaMemsetAsync(dBar_, 0, sizeof(unsigned), stream_));
   tic(KC_PASS);
   cudaError_t e = cudaSuccess;
@@ -664,7 +662,12 @@ int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_
   int iter = 0, last_eval = 0, ma = m, n_evals = 0;
   long long node_its = 0;
   int rc = 0;
-  if (pass_grid_ > 0 && (res_.on || m <= 2 * sms_)) {
+  // The persistent kernel wins when an iteration is latency-bound (narrow
+  // batches, X resident); when one iteration's X V + X'R is large (c4-sized
+  // X), the standalone GEMM kernels (two CTAs per SM) run faster and launch
+  // gaps no longer matter.
+  const double iter_flops = 4.0 * n * (double)p * m;
+  if (pass_grid_ > 0 && (res_.on || (m <= 2 * sms_ && iter_flops <= persist_max_flops_))) {
     // narrow batch: the whole relaxation as one persistent cooperative kernel
     if ((rc = run_pass(m, cfg, thr, eta, rho, dTrace, iter, n_evals, node_its))) goto done;
   } else {

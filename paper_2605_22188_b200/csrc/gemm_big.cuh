@@ -30,17 +30,20 @@ constexpr int kBigB = kBigBN * kBigLDK;
 constexpr int kBigStage = kBigA + kBigB;
 constexpr size_t kBigSmemBytes = sizeof(double) * (size_t)kBigNS * kBigStage;
 
-// One 128 x 64 output tile (row tile mt, column tile nt).  All 256 threads of
-// the CTA call; smem holds kBigSmemBytes; colmap kBigBN ints and epi_red
+// One 128 x BN output tile (row tile mt, column tile nt), BN = 64 (warp tile
+// 32 x 32) or 32 (warp tile 32 x 16, for narrower batches).  All 256 threads
+// of the CTA call; smem holds kBigSmemBytes; colmap kBigBN ints and epi_red
 // 2 x 4 x kBigBN doubles of shared memory.  Ends with a block barrier.
-template <bool TN, int EPI>
+template <bool TN, int EPI, int BN = kBigBN>
 __device__ void gemm_big_tile(const GemmArgs& g, int ncols, int mt, int nt, double* smem,
                               int* colmap, double (*epi_red)[4][kBigBN]) {
-  const int n0 = nt * kBigBN;
+  static_assert(BN == 64 || BN == 32, "BN");
+  constexpr int FN = BN / 16, WN = BN / 2;  // fragments and columns per warp
+  const int n0 = nt * BN;
   const int m0 = mt * kBigBM;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 3, wn = warp >> 2;
-  if (tid < kBigBN) {
+  if (tid < BN) {
     const int c = n0 + tid;
     colmap[tid] = c < ncols ? (g.act ? g.act[c] : c) : -1;
   }
@@ -70,10 +73,11 @@ __device__ void gemm_big_tile(const GemmArgs& g, int ncols, int mt, int nt, doub
         cp_async_16(As + k * kBigLDA_NN + mc, ok ? g.A + (size_t)gk * g.lda + gm : g.A, ok ? 16 : 0);
       }
     }
-    // B: 64 columns x BK
+    // B: BN columns x BK
 #pragma unroll
-    for (int it = 0; it < kBigBN * kBigBK / 2 / kBigThreads; ++it) {
+    for (int it = 0; it < (BN * kBigBK / 2 + kBigThreads - 1) / kBigThreads; ++it) {
       const int e = tid + it * kBigThreads;
+      if (e >= BN * KC) break;
       const int c = e / KC, kc = (e % KC) * 2;
       const int col = colmap[c];
       const int gk = k0 + kc;
@@ -82,11 +86,11 @@ __device__ void gemm_big_tile(const GemmArgs& g, int ncols, int mt, int nt, doub
     }
   };
 
-  double acc[4][4][2];
+  double acc[4][FN][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
   for (int s = 0; s < kBigNS - 1; ++s) {
@@ -103,36 +107,36 @@ __device__ void gemm_big_tile(const GemmArgs& g, int ncols, int mt, int nt, doub
 #pragma unroll
     for (int ks = 0; ks < kBigBK / 4; ++ks) {
       const int kk = ks * 4 + (lane & 3);
-      double a[4], b[4];
+      double a[4], b[FN];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int row = wm * 32 + i * 8 + (lane >> 2);
         a[i] = TN ? As[row * kBigLDK + kk] : As[kk * kBigLDA_NN + row];
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[(wn * 32 + j * 8 + (lane >> 2)) * kBigLDK + kk];
+      for (int j = 0; j < FN; ++j) b[j] = Bs[(wn * WN + j * 8 + (lane >> 2)) * kBigLDK + kk];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int j = 0; j < FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
   }
   cp_async_wait<0>();
 
   // epilogue: lane holds D[row][col] for row = wm*32 + i*8 + lane/4 and
   // col = wn*32 + j*8 + 2*(lane%4) + h
-  double lsum[4][2], csum[4][2];
+  double lsum[FN][2], csum[FN][2];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) lsum[j][0] = lsum[j][1] = csum[j][0] = csum[j][1] = 0.0;
+  for (int j = 0; j < FN; ++j) lsum[j][0] = lsum[j][1] = csum[j][0] = csum[j][1] = 0.0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int gm = m0 + wm * 32 + i * 8 + (lane >> 2);
     const double yv = (EPI != EPI_STORE && gm < g.M) ? g.y[gm] : 0.0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < FN; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int c = wn * 32 + j * 8 + (lane & 3) * 2 + h;
+        const int c = wn * WN + j * 8 + (lane & 3) * 2 + h;
         const int col = colmap[c];
         if (gm >= g.M || col < 0) continue;
         const double s = acc[i][j][h];
@@ -152,7 +156,7 @@ __device__ void gemm_big_tile(const GemmArgs& g, int ncols, int mt, int nt, doub
     // column sums over the CTA's 128 rows: lanes sharing lane%4 (8 rows each),
     // then the 4 warp rows in order
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < FN; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -162,16 +166,16 @@ __device__ void gemm_big_tile(const GemmArgs& g, int ncols, int mt, int nt, doub
         }
     if (lane < 4) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < FN; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int c = wn * 32 + j * 8 + lane * 2 + h;
+          const int c = wn * WN + j * 8 + lane * 2 + h;
           epi_red[0][wm][c] = lsum[j][h];
           epi_red[1][wm][c] = csum[j][h];
         }
     }
     __syncthreads();
-    if (tid < kBigBN && colmap[tid] >= 0) {
+    if (tid < BN && colmap[tid] >= 0) {
       double sl = 0.0, sc = 0.0;
 #pragma unroll
       for (int w = 0; w < 4; ++w) {

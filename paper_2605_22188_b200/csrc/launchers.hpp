@@ -42,7 +42,7 @@ struct PassArgs {
   unsigned* bar;             // grid barrier counter (zeroed before the launch)
   ResLayout res;
   int big;                   // streaming mode: 128 x 64 register-tiled GEMM tiles when
-                             // m_a >= 64 (gemm_big.cuh; needs n, p even)
+                             // m_a >= big (gemm_big.cuh; needs n, p even); 0: never
 };
 
 // ---- gemm_kernels.cu -------------------------------------------------------

@@ -62,8 +62,12 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target) {
 // ---------------------------------------------------------------------------
 // streaming-mode phases
 // ---------------------------------------------------------------------------
-// streaming mode uses the 128 x 64 register-tiled GEMM tiles for wide batches
-__device__ __forceinline__ bool pass_big(const PassArgs& a, int ma) { return a.big && ma >= 64; }
+// streaming mode uses the register-tiled GEMM tiles for wide batches: 128 x 64
+// from kBigNarrowMax active columns on, 128 x 32 below
+constexpr int kBigNarrowMax = 48;
+__device__ __forceinline__ bool pass_big(const PassArgs& a, int ma) {
+  return a.big > 0 && ma >= a.big;
+}
 
 template <int EPI>
 __device__ void pass_phase_nn(const PassArgs& a, const double* Bsrc, int ma, double* smem,
@@ -72,10 +76,17 @@ __device__ void pass_phase_nn(const PassArgs& a, const double* Bsrc, int ma, dou
   g.B = Bsrc;
   g.act = act;
   if (pass_big(a, ma)) {
-    const int mt = (a.n + kBigBM - 1) / kBigBM, nt = (ma + kBigBN - 1) / kBigBN;
     auto* epi = reinterpret_cast<double(*)[4][kBigBN]>(smem + kBigSmemBytes / sizeof(double));
-    for (int t = blockIdx.x; t < mt * nt; t += gridDim.x)
-      gemm_big_tile<false, EPI>(g, ma, t % mt, t / mt, smem, colmap, epi);
+    const int mt = (a.n + kBigBM - 1) / kBigBM;
+    if (ma >= kBigNarrowMax) {
+      const int nt = (ma + kBigBN - 1) / kBigBN;
+      for (int t = blockIdx.x; t < mt * nt; t += gridDim.x)
+        gemm_big_tile<false, EPI, 64>(g, ma, t % mt, t / mt, smem, colmap, epi);
+    } else {
+      const int nt = (ma + 31) / 32;
+      for (int t = blockIdx.x; t < mt * nt; t += gridDim.x)
+        gemm_big_tile<false, EPI, 32>(g, ma, t % mt, t / mt, smem, colmap, epi);
+    }
     return;
   }
   const int fn = pass_fn(ma);
@@ -98,10 +109,17 @@ __device__ inline int pass_phase_tn(const PassArgs& a, int ma, double* smem, int
   GemmArgs g = a.tn;
   g.act = act;
   if (pass_big(a, ma)) {
-    const int mt = (a.p + kBigBM - 1) / kBigBM, nt = (ma + kBigBN - 1) / kBigBN;
     auto* epi = reinterpret_cast<double(*)[4][kBigBN]>(smem + kBigSmemBytes / sizeof(double));
-    for (int t = blockIdx.x; t < mt * nt; t += gridDim.x)
-      gemm_big_tile<true, EPI_STORE>(g, ma, t % mt, t / mt, smem, colmap, epi);
+    const int mt = (a.p + kBigBM - 1) / kBigBM;
+    if (ma >= kBigNarrowMax) {
+      const int nt = (ma + kBigBN - 1) / kBigBN;
+      for (int t = blockIdx.x; t < mt * nt; t += gridDim.x)
+        gemm_big_tile<true, EPI_STORE, 64>(g, ma, t % mt, t / mt, smem, colmap, epi);
+    } else {
+      const int nt = (ma + 31) / 32;
+      for (int t = blockIdx.x; t < mt * nt; t += gridDim.x)
+        gemm_big_tile<true, EPI_STORE, 32>(g, ma, t % mt, t / mt, smem, colmap, epi);
+    }
     return 1;
   }
   const int fn = pass_fn(ma);

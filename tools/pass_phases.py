@@ -13,15 +13,17 @@ import paper_2605_22188_b200 as P  # noqa: E402
 from bench import CONFIGS  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
+limit = float(sys.argv[sys.argv.index("--limit") + 1]) if "--limit" in sys.argv else float("inf")
 n, p, k, rho, loss, _ = CONFIGS[name]
 inst, _ = P.generate_synthetic(P.GeneratorSpec(n=n, p=p, k=k, correlation=rho, loss=loss, seed=0))
 with P.Engine(inst) as eng:
-    eng.solve()
+    cfg = P.SolverConfig(time_limit=limit)
+    eng.solve(cfg)
     before = eng.pass_profile()
     eng.set_timing(True)
     s0 = eng.kernel_stats()
     t0 = time.perf_counter()
-    cert = eng.solve()
+    cert = eng.solve(cfg)
     wall = time.perf_counter() - t0
     s1 = eng.kernel_stats()
     after = eng.pass_profile()
