@@ -64,7 +64,10 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target) {
 // ---------------------------------------------------------------------------
 // streaming mode uses the register-tiled GEMM tiles for wide batches: 128 x 64
 // from kBigNarrowMax active columns on, 128 x 32 below
-constexpr int kBigNarrowMax = 48;
+#ifndef BNBG_NARROW_MAX
+#define BNBG_NARROW_MAX 48
+#endif
+constexpr int kBigNarrowMax = BNBG_NARROW_MAX;
 __device__ __forceinline__ bool pass_big(const PassArgs& a, int ma) {
   return a.big > 0 && ma >= a.big;
 }
