@@ -225,12 +225,16 @@ __device__ void res_tile(const GemmArgs& g, const double* Ares, int lda, int K, 
   // B chunk: 16-byte copies when the rows are 16-byte aligned (even ld and
   // offset), else 8-byte; rows past kvalid are zero-filled
   if (((g.ldb | kbeg) & 1) == 0 && ((reinterpret_cast<size_t>(g.B) & 15) == 0)) {
+    // NT / BN threads per column: no integer division in the issue loop
+    constexpr int TPC = NT / BN;
     const int K2 = K >> 1;
-    for (int e = tid; e < BN * K2; e += NT) {
-      const int c = e / K2, k = 2 * (e - c * K2);
-      const int col = colmap[c];
+    const int c = tid / TPC, col = colmap[c];
+    const double* src = col >= 0 ? g.B + (size_t)col * g.ldb + kbeg : g.B;
+    double* dst = Bs + c * ldb;
+    for (int k2 = tid % TPC; k2 < K2; k2 += TPC) {
+      const int k = 2 * k2;
       const int nb = col < 0 ? 0 : (k + 2 <= kvalid ? 16 : (k < kvalid ? 8 : 0));
-      cp_async_16(Bs + c * ldb + k, nb ? g.B + (size_t)col * g.ldb + kbeg + k : g.B, nb);
+      cp_async_16(dst + k, nb ? src + k : g.B, nb);
     }
   } else {
     for (int c = 0; c < BN; ++c) {
