@@ -54,7 +54,7 @@ int main() {
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     long long st[6]; cudaMemcpy(st, dst, 48, cudaMemcpyDeviceToHost);
     long long pr[8]; cudaMemcpyFromSymbol(pr, g_probe, sizeof(pr));
-    printf("  pava probes: scan %lld, setup %lld, batches %lld, final %lld\n", pr[1]-pr[0], pr[2]-pr[1], pr[3]-pr[2], pr[4]-pr[3]);
+    printf("  pava probes: scan %lld, walk %lld, final %lld\n", pr[1]-pr[0], pr[3]-pr[1], pr[4]-pr[3]);
     printf("p=%d n2=%d: load %lld sort %lld pava %lld scatter %lld cycles; lo=%lld hi=%lld; kernel %.2f us  err=%s\n", p, n2, st[0], st[1], st[2], st[3], st[4], st[5], ms * 1e3, cudaGetErrorString(cudaGetLastError()));
   }
 }
