@@ -175,3 +175,17 @@ def test_config_c5_rashomon_matches_oracle(bnb):
     assert [s for s, _, _ in res.pool] == [m["sequence"] for m in ref["pool"]]
     np.testing.assert_allclose([o for _, _, o in res.pool], [m["objective"] for m in ref["pool"]],
                                rtol=REL)
+
+
+@pytest.mark.parametrize("n,p,k,rho", [(7, 3, 1, 0.3), (33, 17, 17, 0.5), (50, 1, 1, 0.0),
+                                       (101, 33, 5, 0.9), (15, 9, 4, 0.7)])
+@pytest.mark.parametrize("loss", [0, 1])
+def test_edge_shapes_match_oracle(bnb, orc, n, p, k, rho, loss):
+    """Odd n and p (unaligned rows, padded tiles), k = p, p = 1, n < 16."""
+    inst = _inst(bnb, n, p, k, rho, loss, seed=n + p)
+    oi = orc.generate(n, p, k, rho, loss, 5.0, n + p)
+    cert = bnb.solve(inst)
+    ref = orc.solve(oi)
+    assert cert.status == "optimal" and cert.support == ref.support
+    assert abs(cert.optimal_value - ref.optimal_value) <= REL * max(1.0, abs(ref.optimal_value))
+    assert cert.nodes_processed == ref.nodes_processed
