@@ -212,7 +212,6 @@ def main():
         run_reference(args, spec, rank)
         return
 
-    import numpy as np
     import torch
     import paper_2605_22188_b200 as P
 

@@ -203,7 +203,6 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
             bnbg::Comm* comm = nullptr) {
   bnbg::Engine& eng = h->eng;
   const int n = eng.n, p = eng.p, k = eng.k;
-  const double M = eng.M;
   const auto wall_start = Clock::now();
   auto elapsed = [&]() { return std::chrono::duration<double>(Clock::now() - wall_start).count(); };
   cert->optimal_value = kInf;

@@ -16,7 +16,6 @@ from __future__ import annotations
 import ctypes as C
 from typing import Optional
 
-import numpy as np
 
 from . import _lib as _L
 
