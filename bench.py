@@ -200,6 +200,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=120.0)
+    ap.add_argument("--cpu-baseline-only", action="store_true",
+                    help="only the cpu_baseline leg for --config (bounded by --cpu-seconds)")
     ap.add_argument("--time-limit", type=float, default=float("inf"),
                     help="per-certify time limit (c3/c4: nodes/s at a stated limit)")
     args = ap.parse_args()
@@ -210,6 +212,11 @@ def main():
 
     if args.impl == "reference":
         run_reference(args, spec, rank)
+        return
+    if args.cpu_baseline_only:
+        if rank == 0:
+            print(json.dumps({"config": args.config, "cpu_baseline": cpu_baseline(spec, args)}),
+                  flush=True)
         return
 
     import torch
