@@ -25,10 +25,17 @@ this module              reference
 ``prox_step``            prox_kernel.hpp:284-301
 ``batched_conjugate_prox``         prox_kernel.hpp:214-229
 ``g_value`` / ``g_conjugate_value``  prox_kernel.hpp:374-387
+``Engine.pool_root`` / ``pool_relax`` / ``pool_branch``  the device-resident per-pass
+                         seam (bnb_engine.hpp:140, :188-206, :243-255)
+``solve_sharded``        node-parallel solving over GPUs (new)
+``io.load_csv`` / ``io.save_csv``  problem.hpp:208-288
+``io.certificate_to_json``         serialize.hpp:40-64
+``io.file_fingerprint``            serialize.hpp:149-161
 =======================  ==========================================================
 
 Errors: ``InputError`` (input_error), ``NumericError`` (numeric_error),
-``LogicError`` (std::logic_error), ``CudaError`` (new; no CPU fallback exists).
+``LogicError`` (std::logic_error), ``io.ParseError`` (parse_error), ``CudaError``
+(new; no CPU fallback exists).
 """
 from __future__ import annotations
 
