@@ -928,6 +928,7 @@ int Engine::pass_profile(double* ns, int count) {
   CK(cudaMemcpy(h, dPassProf_, sizeof(h), cudaMemcpyDeviceToHost));
   // [0..6] phase totals, [8..14] CTA 0's time to the phase barrier,
   // [16..19] prox sub-phases of CTA 0 (load+sort, PAVA, scatter, barrier)
+  // [28..29] PAVA sub-phases of CTA 0 (scan, walk), [30] walk steps, [31] walks
   const int c = std::min(count, 32);
   for (int i = 0; i < c; ++i) ns[i] = (double)h[i];
   return c;

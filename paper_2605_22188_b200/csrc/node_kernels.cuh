@@ -243,13 +243,15 @@ __device__ __forceinline__ void column_sort(int p, int n2, KF kf, double* key, i
 // ---------------------------------------------------------------------------
 template <int NT>
 __device__ void block_pava(const double* key, int pf, int kbar, double w, double M, double* scan,
-                           int& blo, int& bhi, double& bval) {
+                           int& blo, int& bhi, double& bval, unsigned long long* probe = nullptr) {
   blo = 0;
   bhi = -1;
   bval = 0.0;
   if (kbar <= 0 || kbar >= pf) return;
   if (d_prox_huber(key[kbar - 1], w, M) >= key[kbar]) return;
   BNBG_PAVA_PROBE(0);
+  // sub-phase timers of CTA 0 (scan, walk) and walk statistics (steps, calls)
+  ColProbe pp(probe);
   constexpr int NW = NT / 32;
   __shared__ double s_ftot[NW], s_btot[NW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -292,6 +294,7 @@ __device__ void block_pava(const double* key, int pf, int kbar, double w, double
     __syncthreads();
   BNBG_PAVA_PROBE(1);
   }
+  pp.mark(0);
   // Values are kept as fractions num/den (den > 0) so the expansion tests
   // need no division: pooled(lo,hi) = prox_huber(S/len, w(kbar-lo)/len, M)
   // = S/(len + W) inside the box (|S| <= (len + W) M, W = w (kbar-lo)) and
@@ -329,7 +332,9 @@ __device__ void block_pava(const double* key, int pf, int kbar, double w, double
   int lo = kbar - 1, hi = kbar;
   if (warp == 0) {
     bool left_phase = true;
+    unsigned steps = 0;
     for (;;) {
+      ++steps;
       bool L = false, R = false, ev;
       if (left_phase) {  // state t = (lo - t, hi)
         const int cl = lo - lane;
@@ -375,12 +380,17 @@ __device__ void block_pava(const double* key, int pf, int kbar, double w, double
       s_lohi[0] = lo;
       s_lohi[1] = hi;
     }
+    if (pp.p) {
+      atomicAdd(pp.p + 2, (unsigned long long)steps);
+      atomicAdd(pp.p + 3, 1ull);
+    }
   }
   __syncthreads();
   lo = s_lohi[0];
   hi = s_lohi[1];
   blo = lo;
   bhi = hi;
+  pp.mark(1);
   BNBG_PAVA_PROBE(3);
   bval = pooled(lo, hi);
   BNBG_PAVA_PROBE(4);
@@ -531,7 +541,8 @@ __device__ __forceinline__ double prox_column_impl(const RelaxDev& r, int ns, in
   int lo, hi;
   double pooled;
   pr.mark(0);
-  block_pava<kNodeThreads>(S.key, pf, kb, r.rho, r.M, S.scan, lo, hi, pooled);
+  block_pava<kNodeThreads>(S.key, pf, kb, r.rho, r.M, S.scan, lo, hi, pooled,
+                           r.probe ? r.probe + 12 : nullptr);
   pr.mark(1);
   const double inv_rho = 1.0 / r.rho;
   const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * tm * tm));

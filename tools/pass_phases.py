@@ -53,6 +53,10 @@ with P.Engine(inst) as eng:
     names = ("load+sort", "pava", "scatter", "end barrier")
     print("  prox sub-phases (CTA 0, per iteration): " +
           ", ".join(f"{nm} {raw[16 + i] / its_all / 1e3 / 2:.2f} us" for i, nm in enumerate(names)))
+    walks = max(1.0, raw[31])
+    print(f"  pava (CTA 0): {raw[31] / its_all / 2:.2f} walks per iteration, scan "
+          f"{raw[28] / walks / 1e3:.2f} us, walk {raw[29] / walks / 1e3:.2f} us, "
+          f"{raw[30] / walks:.1f} warp steps per walk")
     tn = ("colmap+issue", "load wait", "mma", "reduce+epilogue")
     for nm, base in (("NN", 20), ("TN", 24)):
         print(f"  {nm} resident tile sub-phases (CTA 0, per iteration incl. evals): " +
