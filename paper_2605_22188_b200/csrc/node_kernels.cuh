@@ -21,6 +21,15 @@
 #pragma once
 #include "device_math.cuh"
 
+#ifndef BNBG_PAVA_WA  // PAVA walk window: left x right moves per step
+#define BNBG_PAVA_WA 8
+#endif
+#ifndef BNBG_PAVA_WB
+#define BNBG_PAVA_WB 4
+#endif
+#ifndef BNBG_PAVA_RQ  // right-run states per lane and step
+#define BNBG_PAVA_RQ 2
+#endif
 // Optional timing probe for the PAVA phases (tools/micro); empty in the product.
 #ifndef BNBG_PAVA_PROBE
 #define BNBG_PAVA_PROBE(i)
@@ -301,80 +310,119 @@ __device__ void block_pava(const double* key, int pf, int kbar, double w, double
   // (S - W M)/len outside (S >= 0: keys are magnitudes); head values
   // v_r = prox_huber(key_r, w, M) likewise.  Only the final pooled value is
   // divided out (prox_kernel.hpp:145-151 evaluates the same quantity).
-  struct Frac {
-    double num, den;
+  // Left and right tests of state (cl, ch), branch-free so that several
+  // states per lane overlap their loads (indices clamped; states outside
+  // [0, pf) test false and are never reached).  v(cl-1) is always a head
+  // value (cl <= kbar - 1) and v(ch+1) a raw key (ch >= kbar).
+  const double hb = (1.0 + w) * M, wM = w * M;
+  auto test = [&](int cl, int ch, bool& L, bool& R) {
+    const bool ok = cl >= 0 && ch <= pf - 1;
+    const int c0 = max(cl, 0), c1 = min(ch, pf - 1);
+    const double len = (double)(c1 - c0 + 1);
+    const double S = SL[kbar - 1 - c0] + SR[c1 - kbar];
+    const double W = w * (double)(kbar - c0);
+    const bool box = S <= (len + W) * M;
+    const double pn = box ? S : S - W * M, pd = box ? len + W : len;
+    const double a = key[max(c0 - 1, 0)];
+    const bool hbox = a <= hb;
+    const double vn = hbox ? a : a - wM, vd = hbox ? 1.0 + w : 1.0;
+    const double b = key[min(c1 + 1, pf - 1)];
+    L = ok && c0 > 0 && vn * pd < pn * vd;
+    R = ok && c1 < pf - 1 && pn * 1.0 < b * pd;
   };
-  auto pooled_f = [&](int lo, int hi) {
-    const double len = (double)(hi - lo + 1);
-    const double S = SL[kbar - 1 - lo] + SR[hi - kbar];
-    const double W = w * (double)(kbar - lo);
-    if (S <= (len + W) * M) return Frac{S, len + W};
-    return Frac{S - W * M, len};
-  };
-  auto v_f = [&](int r) {
-    const double a = key[r];
-    if (r >= kbar) return Frac{a, 1.0};
-    if (a <= (1.0 + w) * M) return Frac{a, 1.0 + w};
-    return Frac{a - w * M, 1.0};
-  };
-  auto less = [](const Frac& x, const Frac& y) { return x.num * y.den < y.num * x.den; };
   auto pooled = [&](int lo, int hi) {
     const int len = hi - lo + 1;
     const double sum = SL[kbar - 1 - lo] + SR[hi - kbar];
     const double mean_w = w * (double)(kbar - lo) / len;
     return d_prox_huber(sum / len, mean_w, M);
   };
-  // The expansion is replayed by warp 0 alone, 32 consecutive states per
-  // step (no block barrier inside the walk): a left run tests (lo - t, hi),
-  // a right run (lo, hi + t); the first state that ends the run is located
-  // with a ballot, in the reference's decision order (left test first).
+  // The expansion is replayed by warp 0 alone (no block barrier inside the
+  // walk).  From state (lo, hi) the reference moves left while the left test
+  // fires, else right while the right test fires, else stops; each step
+  // evaluates a window of states in one pass:
+  //  - 2-D window: lane (a, b) < (WA, WB) tests state (lo - a, hi + b); the
+  //    path through the window is traced from the ballots of both tests;
+  //  - after a window left by a straight run, a 1-D run along it (left:
+  //    (lo - t, hi), 32 states; right: (lo, hi + t), 32 * RQ states), ending
+  //    at the first state whose decision differs.
+  // Both follow the reference's decision order exactly (left test first).
+  // Left moves number at most kbar - 1, so long walks are right runs.
+  constexpr int WA = BNBG_PAVA_WA, WB = BNBG_PAVA_WB, RQ = BNBG_PAVA_RQ;
+  static_assert(WA * WB <= 32, "PAVA window");
   __shared__ int s_lohi[2];
   int lo = kbar - 1, hi = kbar;
   if (warp == 0) {
-    bool left_phase = true;
+    int mode = 0;  // 0: 2-D window, 1: left run, 2: right run
     unsigned steps = 0;
+    const int la = lane / WB, lb = lane - (lane / WB) * WB;
     for (;;) {
       ++steps;
-      bool L = false, R = false, ev;
-      if (left_phase) {  // state t = (lo - t, hi)
-        const int cl = lo - lane;
-        if (cl >= 0) {
-          const Frac pv = pooled_f(cl, hi);
-          L = cl > 0 && less(v_f(cl - 1), pv);
-          R = hi < pf - 1 && less(pv, v_f(hi + 1));
+      if (mode == 0) {
+        bool L, R;
+        test(lo - la, hi + lb, L, R);
+        L = L && lane < WA * WB;
+        R = R && lane < WA * WB;
+        const unsigned bl = __ballot_sync(0xffffffffu, L);
+        const unsigned br = __ballot_sync(0xffffffffu, R);
+        int a = 0, b = 0, idx = 0;
+        bool done = false;
+        for (;;) {
+          if ((bl >> idx) & 1u) {
+            if (++a == WA) break;
+            idx += WB;
+          } else if ((br >> idx) & 1u) {
+            if (++b == WB) break;
+            ++idx;
+          } else {
+            done = true;
+            break;
+          }
         }
-        ev = !L;
-      } else {  // state t = (lo, hi + t)
-        const int ch = hi + lane;
-        if (ch <= pf - 1) {
-          const Frac pv = pooled_f(lo, ch);
-          L = lo > 0 && less(v_f(lo - 1), pv);
-          R = ch < pf - 1 && less(pv, v_f(ch + 1));
-        }
-        ev = L || !R;
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, ev);
-      if (!bal) {
-        if (left_phase)
-          lo -= 32;
-        else
-          hi += 32;
+        lo -= a;
+        hi += b;
+        if (done) break;
+        mode = b == 0 ? 1 : (a == 0 ? 2 : 0);
         continue;
       }
-      const int first = __ffs(bal) - 1;
-      const bool Lf = __shfl_sync(0xffffffffu, L, first);
-      const bool Rf = __shfl_sync(0xffffffffu, R, first);
-      if (left_phase) {
+      if (mode == 1) {  // state t = (lo - t, hi): runs while L
+        bool L, R;
+        test(lo - lane, hi, L, R);
+        const unsigned bev = __ballot_sync(0xffffffffu, !L);
+        const unsigned br = __ballot_sync(0xffffffffu, R);
+        if (!bev) {
+          lo -= 32;
+          continue;
+        }
+        const int first = __ffs(bev) - 1;
         lo -= first;
-        if (!Rf) break;
+        if (!((br >> first) & 1u)) break;
         ++hi;
-        left_phase = false;
-      } else {
-        hi += first;
-        if (!Lf) break;
-        --lo;
-        left_phase = true;
+        mode = 0;
+        continue;
       }
+      // state t = (lo, hi + t) for t = q * 32 + lane: runs while !L && R
+      unsigned bev[RQ], bl[RQ];
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) {
+        bool L, R;
+        test(lo, hi + q * 32 + lane, L, R);
+        bev[q] = __ballot_sync(0xffffffffu, L || !R);
+        bl[q] = __ballot_sync(0xffffffffu, L);
+      }
+      int adv = 32 * RQ;
+      bool Lf = false;
+#pragma unroll
+      for (int q = RQ - 1; q >= 0; --q)
+        if (bev[q]) {
+          const int f = __ffs(bev[q]) - 1;
+          adv = q * 32 + f;
+          Lf = (bl[q] >> f) & 1u;
+        }
+      hi += adv;
+      if (adv == 32 * RQ) continue;
+      if (!Lf) break;
+      --lo;
+      mode = 0;
     }
     if (lane == 0) {
       s_lohi[0] = lo;
