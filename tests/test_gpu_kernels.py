@@ -45,6 +45,37 @@ def test_prox_step_matches_oracle(bnb, orc, p, m, k):
         np.testing.assert_allclose(out, ref, rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("shape", ["plateau", "ramp", "ties", "heads_out_of_box"])
+@pytest.mark.parametrize("p,k", [(100, 5), (500, 8), (2000, 15)])
+def test_prox_long_pava_walks(bnb, orc, shape, p, k):
+    """Key layouts that drive the PAVA walk through long right runs (more
+    than one 64-state step), alternating left/right moves across the 2-D
+    window, exact ties (rank order by index) and head values outside the box."""
+    rng = np.random.default_rng(p + k)
+    m = 4
+    if shape == "plateau":
+        U = 1.0 + 1e-3 * rng.normal(size=(p, m))
+    elif shape == "ramp":
+        U = np.linspace(3.0, 0.5, p)[:, None] * (1.0 + 1e-6 * rng.normal(size=(p, m)))
+    elif shape == "ties":
+        U = rng.choice([0.7, 0.7, 0.69, 0.5], size=(p, m))
+    else:
+        U = rng.normal(size=(p, m)) * 0.2
+        U[:k, :] = 9.0 + rng.random(size=(k, m))
+    U *= rng.choice([-1.0, 1.0], size=(p, m))
+    st = np.zeros((p, m), dtype=np.uint8)
+    st[rng.permutation(p)[: p // 10], 1] = 2  # fixed-zero coordinates in one column
+    st[0, 2] = 1                              # one fixed-one coordinate
+    kb = [k, k, k - 1, 1]
+    for eta in (0.05, 0.5):
+        out = bnb.prox_step(U, eta, 1.0, st, kb, 2.0)
+        rho = 1.0 / (2 * eta)
+        ref = np.stack([orc.prox_step_column(U[:, b], st[:, b], kb[b], rho, 2.0)
+                        for b in range(m)], 1)
+        assert np.array_equal(out == 0.0, ref == 0.0)
+        np.testing.assert_allclose(out, ref, rtol=1e-12, atol=1e-12)
+
+
 def test_prox_golden_vectors(bnb):
     """Committed oracle vectors (tests/golden/prox_vectors.json)."""
     with open(os.path.join(GOLDEN, "prox_vectors.json")) as f:

@@ -1,6 +1,8 @@
 """Summarise `ncu --set full` captures into profiles/ncu_summary.json.
 
-python tools/ncu_summary.py CLASS=path.ncu-rep [CLASS=path.ncu-rep ...] [--out profiles/ncu_summary.json]
+python tools/ncu_summary.py CLASS=path.ncu-rep[@i] [CLASS=path.ncu-rep ...] [--out profiles/ncu_summary.json]
+
+@i selects the i-th captured launch of a report (default the first).
 
 CLASS is the bench kernel class ("pass", "reopt", ...); bench.py reads
 `dram_bytes_per_launch` of the dominant class as roofline.traffic.
@@ -42,10 +44,14 @@ SCALE = {"byte/second": 1, "Kbyte/second": 1e3, "Mbyte/second": 1e6, "Gbyte/seco
 
 
 def summarise(path):
+    idx = 0
+    if "@" in path:  # path@i: the i-th captured launch of the report
+        path, i = path.rsplit("@", 1)
+        idx = int(i)
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units, vals = rows[0], rows[1], rows[2 + idx]
     d = {"kernel": vals[hdr.index("Kernel Name")], "source": os.path.basename(path)}
     for m, key in METRICS.items():
         if m not in hdr:
