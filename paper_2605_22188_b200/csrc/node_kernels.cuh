@@ -270,8 +270,10 @@ __device__ void block_pava(const double* key, int pf, int kbar, double w, double
     const int chunk = (pf + NT - 1) / NT;
     const int beg = min(pf, tid * chunk), end = min(pf, beg + chunk);
     double f = 0.0, bsum = 0.0;
+#pragma unroll 2
     for (int r = beg; r < end; ++r)
       if (r >= kbar) f += key[r];
+#pragma unroll 2
     for (int r = end - 1; r >= beg; --r)
       if (r < kbar) bsum += key[r];
     double fi = f, bi = bsum;  // inclusive warp scans: forward (up), backward (down)
@@ -286,15 +288,27 @@ __device__ void block_pava(const double* key, int pf, int kbar, double w, double
     if (lane == 0) s_btot[warp] = bi;
     __syncthreads();
     double foff = fi - f, boff = bi - bsum;
-    for (int w2 = 0; w2 < warp; ++w2) foff += s_ftot[w2];
-    for (int w2 = NW - 1; w2 > warp; --w2) boff += s_btot[w2];
+    // warp offsets in the same order as a loop to `warp`, with the loads
+    // issued together (adding nothing for the other warps)
+#pragma unroll
+    for (int w2 = 0; w2 < NW; ++w2) {
+      const double v = s_ftot[w2];
+      if (w2 < warp) foff += v;
+    }
+#pragma unroll
+    for (int w2 = NW - 1; w2 >= 0; --w2) {
+      const double v = s_btot[w2];
+      if (w2 > warp) boff += v;
+    }
     double run = foff;
+#pragma unroll 2
     for (int r = beg; r < end; ++r)
       if (r >= kbar) {
         run += key[r];
         SR[r - kbar] = run;
       }
     run = boff;
+#pragma unroll 2
     for (int r = end - 1; r >= beg; --r)
       if (r < kbar) {
         run += key[r];
