@@ -397,39 +397,41 @@ int Engine::compute_smoothness(double* out) {
   int nsplit = std::max(1, std::min(32, (2 * sms_ + row_blocks - 1) / row_blocks));
   const int chunk = (p + nsplit - 1) / nsplit;
   nsplit = (p + chunk - 1) / chunk;
-  if (int rc = ensure_aux(sizeof(double) * ((size_t)2 * p + n + 2 + (size_t)nsplit * n))) return rc;
+  if (int rc = ensure_aux(sizeof(double) * ((size_t)2 * p + n + 2 + (size_t)nsplit * n + 4)))
+    return rc;
   double* dv = static_cast<double*>(dAux_);
   double* dw = dv + p;
   double* dxv = dw + p;
   double* dstat = dxv + n;
   double* dpart = dstat + 2;
+  double* dps = dpart + (size_t)nsplit * n;  // {done, estimate, result, rounds}
   if (int rc_ = h2d(dv, v.data(), sizeof(double) * p)) return rc_;
-  double estimate = 0.0, stats[2];
-  double result = -1.0;
-  for (int it = 0; it < 100; ++it) {
-    k_gemv_n_part<<<dim3(row_blocks, nsplit), 256, 0, stream_>>>(n, p, chunk, dX_, dv, dpart);
-    CKL("k_gemv_n_part");
-    k_gemv_n_sum<<<row_blocks, 256, 0, stream_>>>(n, nsplit, dpart, dxv);
-    CKL("k_gemv_n_sum");
-    k_gemv_t<<<(p + 7) / 8, 256, 0, stream_>>>(n, p, dX_, dxv, dw);
-    CKL("k_gemv_t");
-    k_power_stats<<<1, 256, 0, stream_>>>(p, dv, dw, dstat);
-    CKL("k_power_stats");
-    if (int rc_ = d2h(stats, dstat, sizeof(stats))) return rc_;
+  const double ps0[4] = {0.0, 0.0, -1.0, 0.0};
+  if (int rc_ = h2d(dps, ps0, sizeof(ps0))) return rc_;
+  // rounds are launched in batches with the stopping test on the device, so
+  // the host synchronises once per batch instead of once per round
+  double ps[4] = {0.0, 0.0, -1.0, 0.0};
+  for (int launched = 0; launched < 100;) {
+    const int batch = std::min(launched == 0 ? 4 : 8, 100 - launched);
+    for (int b = 0; b < batch; ++b) {
+      k_gemv_n_part<<<dim3(row_blocks, nsplit), 256, 0, stream_>>>(n, p, chunk, dX_, dv, dpart, dps);
+      CKL("k_gemv_n_part");
+      k_gemv_n_sum<<<row_blocks, 256, 0, stream_>>>(n, nsplit, dpart, dxv, dps);
+      CKL("k_gemv_n_sum");
+      k_gemv_t<<<(p + 7) / 8, 256, 0, stream_>>>(n, p, dX_, dxv, dw, dps);
+      CKL("k_gemv_t");
+      k_power_stats<<<1, 256, 0, stream_>>>(p, dv, dw, dstat, dps);
+      CKL("k_power_stats");
+      k_power_update<<<1, 256, 0, stream_>>>(p, dw, dstat, dv, dps);
+      CKL("k_power_update");
+    }
+    launched += batch;
+    if (int rc_ = d2h(ps, dps, sizeof(ps))) return rc_;
     CK(cudaStreamSynchronize(stream_));
-    const double next = stats[0], wn = stats[1];
-    if (wn == 0.0 || next <= 0.0) {
-      result = 1e-12;
-      break;
-    }
-    k_scale<<<(p + 255) / 256, 256, 0, stream_>>>(p, dw, wn, dv);
-    CKL("k_scale");
-    if (it > 0 && std::fabs(next - estimate) <= 1e-4 * next) {
-      estimate = next;
-      break;
-    }
-    estimate = next;
+    if (ps[0] != 0.0) break;
   }
+  const double estimate = ps[1];
+  double result = ps[2];
   if (result < 0.0) result = std::max(1.01 * c * estimate, 1e-12);
   *out = result;
   return 0;

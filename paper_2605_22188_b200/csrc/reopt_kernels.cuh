@@ -2,7 +2,7 @@
 //
 //   k_reopt / k_reopt_direct / k_reopt_gram   reoptimize_supports
 //                                  (primal_heuristics.hpp:174-227)
-//   k_gemv_n_part / _sum, k_gemv_t, k_power_stats, k_scale   smoothness_constant
+//   k_gemv_n_part / _sum, k_gemv_t, k_power_stats, k_power_update   smoothness_constant
 //                                  power iteration (losses.hpp:86-112)
 #pragma once
 #include <cooperative_groups.h>
@@ -751,10 +751,13 @@ static __global__ void __launch_bounds__(kReoptFastThreads)
 // --------------------------------------------------------------------------
 // X v split over column chunks (grid.y): partial[s*n + i] over chunk s, summed
 // in chunk order by k_gemv_n_sum -- enough CTAs to cover the SMs at c2 sizes
+// ps = {done, estimate, result, rounds}: once `done` is set on the device the
+// remaining kernels of a launched batch of rounds return at once
 static __global__ void k_gemv_n_part(int n, int p, int chunk, const double* __restrict__ X,
-                                     const double* __restrict__ v, double* __restrict__ part) {
+                                     const double* __restrict__ v, double* __restrict__ part,
+                                     const double* ps) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n || ps[0] != 0.0) return;
   const int j0 = blockIdx.y * chunk, j1 = min(p, j0 + chunk);
   double s = 0.0;
   for (int j = j0; j < j1; ++j) s += X[(size_t)j * n + i] * v[j];
@@ -762,9 +765,9 @@ static __global__ void k_gemv_n_part(int n, int p, int chunk, const double* __re
 }
 
 static __global__ void k_gemv_n_sum(int n, int ns, const double* __restrict__ part,
-                                    double* __restrict__ xv) {
+                                    double* __restrict__ xv, const double* ps) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n || ps[0] != 0.0) return;
   double s = part[i];
   for (int q = 1; q < ns; ++q) s += part[(size_t)q * n + i];
   xv[i] = s;
@@ -772,10 +775,10 @@ static __global__ void k_gemv_n_sum(int n, int ns, const double* __restrict__ pa
 
 
 static __global__ void k_gemv_t(int n, int p, const double* __restrict__ X, const double* __restrict__ xv,
-                         double* __restrict__ w) {
+                         double* __restrict__ w, const double* ps) {
   const int j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (j >= p) return;
+  if (j >= p || ps[0] != 0.0) return;
   const double* col = X + (size_t)j * n;
   double s = 0.0;
   for (int i = lane; i < n; i += 32) s += col[i] * xv[i];
@@ -785,8 +788,10 @@ static __global__ void k_gemv_t(int n, int p, const double* __restrict__ X, cons
 }
 
 // out[0] = v.w, out[1] = |w|; single CTA of 256 threads
-static __global__ void k_power_stats(int p, const double* v, const double* w, double* out) {
+static __global__ void k_power_stats(int p, const double* v, const double* w, double* out,
+                                     const double* ps) {
   __shared__ double red[8];
+  if (ps[0] != 0.0) return;
   double a = 0.0, c = 0.0;
   for (int j = threadIdx.x; j < p; j += 256) {
     a += v[j] * w[j];
@@ -800,9 +805,35 @@ static __global__ void k_power_stats(int p, const double* v, const double* w, do
   }
 }
 
-static __global__ void k_scale(int p, const double* w, double wn, double* v) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < p) v[j] = w[j] / wn;
+// one round's host logic of losses.hpp:96-110 on the device (single CTA):
+// stop on a zero or non-positive estimate (result 1e-12), else v = w/|w|, and
+// stop once the estimate changes by at most 1e-4 relative (after round 0)
+static __global__ void k_power_update(int p, const double* w, const double* stat, double* v,
+                                      double* ps) {
+  __shared__ int s_dec;
+  if (ps[0] != 0.0) return;
+  const double next = stat[0], wn = stat[1];
+  if (threadIdx.x == 0) {
+    int dec = 0;  // 0: continue, 1: zero / non-positive, 2: converged
+    if (wn == 0.0 || next <= 0.0)
+      dec = 1;
+    else if (ps[3] > 0.0 && fabs(next - ps[1]) <= 1e-4 * next)
+      dec = 2;
+    s_dec = dec;
+  }
+  __syncthreads();
+  const int dec = s_dec;
+  if (dec != 1)
+    for (int j = threadIdx.x; j < p; j += blockDim.x) v[j] = w[j] / wn;
+  if (threadIdx.x == 0) {
+    if (dec == 1) {
+      ps[2] = 1e-12;
+    } else {
+      ps[1] = next;
+    }
+    if (dec != 0) ps[0] = 1.0;
+    ps[3] += 1.0;
+  }
 }
 
 

@@ -7,6 +7,14 @@ import json
 import os
 import sys
 
+
+def emit(obj):
+    """One result line per rank in a single write(2): the ranks share the
+    launcher's stdout pipe, and writes below PIPE_BUF do not interleave."""
+    sys.stdout.flush()
+    os.write(1, (json.dumps(obj) + "\n").encode())
+
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
@@ -32,8 +40,7 @@ def host_ops_check():
                            C.cast(rbuf, C.c_void_p), (C.c_int64 * w)(*rb))
     got = list(rbuf.raw)
     exp = [16 * q + r for q in range(w) for _ in range(rb[q])]
-    print(json.dumps({"rank": r, "rc": [rc1, rc2], "allgather": list(recv),
-                      "alltoallv_ok": got == exp}), flush=True)
+    emit({"rank": r, "rc": [rc1, rc2], "allgather": list(recv), "alltoallv_ok": got == exp})
     dist.destroy_process_group()
 
 
@@ -50,9 +57,8 @@ def solve(transport, n, p, k, rho, loss, seed, batch):
     cfg = P.SolverConfig(batch_size=batch) if batch else P.SolverConfig()
     with P.Engine(inst, device=dev) as eng:
         cert = eng.solve_sharded(cfg, transport=transport)
-    print(json.dumps({"rank": dist.get_rank(), "support": cert.support,
-                      "value": cert.optimal_value, "nodes": cert.nodes_processed,
-                      "status": cert.status, "lb_batches": cert.lb_batches}), flush=True)
+    emit({"rank": dist.get_rank(), "support": cert.support, "value": cert.optimal_value,
+          "nodes": cert.nodes_processed, "status": cert.status, "lb_batches": cert.lb_batches})
     dist.destroy_process_group()
 
 
