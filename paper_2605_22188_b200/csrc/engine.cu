@@ -418,7 +418,7 @@ int Engine::compute_smoothness(double* out) {
       CKL("k_gemv_n_part");
       k_gemv_n_sum<<<row_blocks, 256, 0, stream_>>>(n, nsplit, dpart, dxv, dps);
       CKL("k_gemv_n_sum");
-      k_gemv_t<<<(p + 7) / 8, 256, 0, stream_>>>(n, p, dX_, dxv, dw, dps);
+      k_gemv_t<<<(p + 3) / 4, 128, 0, stream_>>>(n, p, dX_, dxv, dw, dps);  // a warp per column
       CKL("k_gemv_t");
       k_power_stats<<<1, 256, 0, stream_>>>(p, dv, dw, dstat, dps);
       CKL("k_power_stats");

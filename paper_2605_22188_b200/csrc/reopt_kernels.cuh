@@ -760,6 +760,7 @@ static __global__ void k_gemv_n_part(int n, int p, int chunk, const double* __re
   if (i >= n || ps[0] != 0.0) return;
   const int j0 = blockIdx.y * chunk, j1 = min(p, j0 + chunk);
   double s = 0.0;
+#pragma unroll 8  // loads issued ahead; the sum keeps its order
   for (int j = j0; j < j1; ++j) s += X[(size_t)j * n + i] * v[j];
   part[(size_t)blockIdx.y * n + i] = s;
 }
@@ -769,6 +770,7 @@ static __global__ void k_gemv_n_sum(int n, int ns, const double* __restrict__ pa
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n || ps[0] != 0.0) return;
   double s = part[i];
+#pragma unroll 8  // loads issued ahead; the sum keeps its order
   for (int q = 1; q < ns; ++q) s += part[(size_t)q * n + i];
   xv[i] = s;
 }
@@ -781,6 +783,7 @@ static __global__ void k_gemv_t(int n, int p, const double* __restrict__ X, cons
   if (j >= p || ps[0] != 0.0) return;
   const double* col = X + (size_t)j * n;
   double s = 0.0;
+#pragma unroll 8  // loads issued ahead; the sum keeps its order
   for (int i = lane; i < n; i += 32) s += col[i] * xv[i];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
