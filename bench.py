@@ -115,15 +115,21 @@ def _load_peaks():
         return {}
 
 
-def _ncu_traffic(kernel_class):
-    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+def _ncu_traffic(kernel_class, config):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    summary, when that capture was taken on this config (its report is named
+    after it, e.g. ncu_gemm_big_c3w.ncu-rep); None otherwise."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(kernel_class, {}).get("dram_bytes_per_launch")
     except (OSError, ValueError):
         return None
+    ent = d.get(f"{kernel_class}@{config}") or d.get(kernel_class, {})
+    src = ent.get("source", "")
+    if f"_{config}." not in src and f"_{config}w." not in src:
+        return None
+    return ent.get("dram_bytes_per_launch")
 
 
 def run_reference(args, spec, rank):
@@ -310,7 +316,7 @@ def main():
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                 "algorithmic": "41*p bytes per node-iteration"}
-    roof["traffic"] = _ncu_traffic(dom)
+    roof["traffic"] = _ncu_traffic(dom, args.config)
     roof["avg_launch_us"] = 1e3 * ms / max(ln, 1)
     roof["share_of_step"] = ms / max(1e-9, 1e3 * prof_cert.profile.total_seconds)
     roof["kernel_ms"] = {kc: round(v[0], 3) for kc, v in delta.items()}
