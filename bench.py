@@ -324,7 +324,10 @@ def main():
     # e2e: the public API from host arrays (instance upload, solve, certificate readback)
     e2e_ms, e2e_nodes, h2d, d2h = 0.0, 0, 0, 0
     e2e_parts = [0.0, 0.0, 0.0]  # create (upload + L), solve, destroy
-    for _ in range(args.steps):
+    # W untimed warm-up rounds first, as for the device-timed steps (the first
+    # create of a process grows the stream-ordered memory pool)
+    for it in range(args.warmup + args.steps):
+        timed = it >= args.warmup
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -336,6 +339,8 @@ def main():
         e2.close()
         torch.cuda.synchronize()
         t3 = time.perf_counter()
+        if not timed:
+            continue
         e2e_parts[0] += t1 - t0
         e2e_parts[1] += t2 - t1
         e2e_parts[2] += t3 - t2

@@ -1,6 +1,9 @@
 // engine.cu -- device engine: instance upload, GEMM planning, the relaxation
 // loop (relaxation.hpp:163-255), rounding/branch selection and re-opt.
 #include <algorithm>
+#include <chrono>
+#include <mutex>
+#include <vector>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -13,6 +16,31 @@
 #include "rng.hpp"
 
 namespace bnbg {
+
+// Small pinned host slots (4 ints) for the per-pass readbacks, kept for the
+// process: page-locking a new block costs ~2 ms per engine creation, which
+// would dominate creating an engine for a small instance.
+static std::mutex g_pin_mu;
+static std::vector<int*> g_pin_free;
+
+static int* pinned_slot_acquire() {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (!g_pin_free.empty()) {
+      int* s = g_pin_free.back();
+      g_pin_free.pop_back();
+      return s;
+    }
+  }
+  void* p = nullptr;
+  if (cudaMallocHost(&p, 64) != cudaSuccess) return nullptr;
+  return static_cast<int*>(p);
+}
+
+static void pinned_slot_release(int* s) {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.push_back(s);
+}
 
 #define CK(call)                                          \
   do {                                                    \
@@ -74,7 +102,7 @@ Engine::~Engine() {
   dfree(dOneLen_);
   dfree(dOneIdx_);
   dfree(dLists_);
-  if (hPin_) cudaFreeHost(hPin_);
+  if (hPin_) pinned_slot_release(hPin_);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -99,8 +127,21 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
   M = M_;
   lambda2 = lambda2_;
   device = device_;
+  // BNBG_INIT_PROF=1: wall time of each creation step on stderr (diagnostics)
+  const char* ip = getenv("BNBG_INIT_PROF");
+  const bool iprof = ip && ip[0] == '1';
+  auto t_last = std::chrono::steady_clock::now();
+  auto stamp = [&](const char* what) {
+    if (!iprof) return;
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "init %-14s %8.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
   CK(cudaSetDevice(device));
+  stamp("set_device");
   CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  stamp("stream");
   {  // stream-ordered allocations: keep freed blocks in the device pool for reuse
     cudaMemPool_t mp;
     CK(cudaDeviceGetDefaultMemPool(&mp, device));
@@ -110,11 +151,14 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
   CK(cudaEventCreate(&ev0_));
   CK(cudaEventCreate(&ev1_));
   CK(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device));
-  CK(cudaMallocHost(&hPin_, 4 * sizeof(int)));
+  hPin_ = pinned_slot_acquire();
+  if (!hPin_) return cuda_fail(cudaErrorMemoryAllocation, "cudaMallocHost");
+  stamp("malloc_host");
   CK(cudaMallocAsync(&dX_, sizeof(double) * (size_t)n * p, stream_));
   CK(cudaMallocAsync(&dy_, sizeof(double) * (size_t)n, stream_));
   if (int rc_ = h2d(dX_, X, sizeof(double) * (size_t)n * p)) return rc_;
   if (int rc_ = h2d(dy_, y, sizeof(double) * (size_t)n)) return rc_;
+  stamp("upload");
   CK(cudaMallocAsync(&dMa_, sizeof(int), stream_));
   CK(cudaMallocAsync(&dErr_, sizeof(int), stream_));
   CK(gemm_set_attrs());
@@ -123,6 +167,7 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
   csmem_ = column_smem_bytes(p, n2_, colE_);
   if (csmem_ > 220 * 1024) return fail(1, "p too large for the column kernels");
   CK(column_set_attrs(colE_, csmem_));
+  stamp("attrs");
   // persistent pass kernel: one CTA per SM when it fits (BNBG_PERSISTENT=0
   // disables it; BNBG_RESIDENT=0 forces the streaming operand mode)
   {
@@ -162,6 +207,7 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
       CK(cudaMemsetAsync(dPassProf_, 0, 32 * sizeof(unsigned long long), stream_));
     }
   }
+  stamp("pass_plan");
   nrb_max_ = (n + 15) / 16;
   {  // per-iteration work above which streaming batches use the standalone kernels
     const char* e = getenv("BNBG_PERSIST_MAXFLOPS");
@@ -186,12 +232,14 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
       return rc;
   }
   CK(cudaStreamSynchronize(stream_));
+  stamp("prealloc+sync");
   if (L_ > 0.0) {
     L = L_;
   } else {
     int rc = compute_smoothness(&L);
     if (rc) return rc;
   }
+  stamp("smoothness");
   return 0;
 }
 
