@@ -7,15 +7,25 @@ regression n=2000, p=500, k=8, rho=0.7, seed 0, M=2, lambda2=1; the other
 configs are parity-test cases).  value = nodes processed / second over the
 timed steps (whole job: all ranks); ms_per_step = time-to-certify.
 
-With N > 1 ranks (torchrun) the same instance is certified by the
+With N > 1 ranks (torchrun) the default workload is c4 (logistic n=20000
+p=5000 k=15, the largest config and the one whose frontier is wide enough to
+shard; c2's 145-node tree is latency-bound and does not), certified by the
 node-sharded solve (bnbg_solve_sharded over NCCL: X replicated, open nodes
 dealt over the GPUs, incumbent / termination / node exchange per pass), so
 the total work is fixed ("scaling": "strong").
 
+At N = 1 the line also carries a `secondary` block for the configs the CPU
+cannot certify: c3 (nodes/s inside a 20 s limit) and c4 (nodes/s inside a
+30 s limit), each with its own clocks, roofline and a cpu_baseline of the
+reference at the same time limit.
+
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
---impl reference times the reference algorithm's CPU implementation (the C
-restatement in oracle/, OpenBLAS DGEMM, all host threads) on rank 0.
+--impl reference times THE REFERENCE ITSELF on rank 0's host cores: the
+unmodified bnbglm headers compiled through the Eigen-subset shim
+(oracle/_ref/libbnbref.so, OpenBLAS DGEMM, workers = all host threads), each
+step one full certify of the same workload ("kind": "reference"); without
+the prebuilt library it falls back to the C restatement (oracle/, "port").
 """
 from __future__ import annotations
 
@@ -132,69 +142,182 @@ def _ncu_traffic(kernel_class, config):
     return ent.get("dram_bytes_per_launch")
 
 
-def run_reference(args, spec, rank):
-    """Reference arm: the CPU implementation of the path on the host cores."""
-    if rank != 0:
-        return
+def _workload(args):
+    return f"{args.config}: {CONFIGS[args.config][5]}, " + (
+        "certify to 0 gap" if math.isinf(args.time_limit)
+        else f"nodes/s within a {args.time_limit:g} s time limit")
+
+
+def config_dict(args):
+    """The `config` object, identical in both arms (b200 and reference)."""
+    n, p, k, rho, loss, desc = CONFIGS[args.config]
+    return {"workload": _workload(args), "n": n, "p": p, "k": k, "rho": rho,
+            "loss": "logistic" if loss else "squared", "seed": 0, "M": 2.0, "lambda2": 1.0,
+            "batch_size": "auto (bnb_engine.hpp:75-88, 1 GiB budget)",
+            "time_limit_s": None if math.isinf(args.time_limit) else args.time_limit,
+            "l2": "b200 arm: flushed (256 MiB write) before every step; reference arm: host"}
+
+
+def _cpu_oracle():
+    """The CPU leg: the reference itself (oracle/_ref) when built, else the
+    C restatement.  Returns (module, kind, threads, blas)."""
     from oracle import oracle as O
-    n, p, k, rho, loss, desc = spec
     O.build()
+    kind = "reference" if O.ref_available() else "port"
+    O.set_backend("ref" if kind == "reference" else "c")
     threads = os.cpu_count() or 1
     blas = O.use_openblas(threads)
+    return O, kind, threads, blas
+
+
+def _cpu_desc(kind, threads, blas):
+    what = ("the reference (bnbglm headers via the Eigen-subset shim, oracle/_ref)"
+            if kind == "reference" else "the reference port (oracle/oracle.c)")
+    return f"{what}, workers={threads}" + (", OpenBLAS DGEMM" if blas else ", C loops")
+
+
+def run_reference(args, spec, rank):
+    """Reference arm: the reference's CPU solver on the host cores, each step
+    one full certify (or one time-limited solve at the arm's --time-limit)."""
+    if rank != 0:
+        return
+    n, p, k, rho, loss, desc = spec
+    O, kind, threads, blas = _cpu_oracle()
     inst = O.generate(n, p, k, rho, loss, 5.0, 0, 2.0, 1.0)
-    cfg_full = O.solver_cfg(workers=threads)
-    # untimed warm-up: bounded 1 s samples
-    for _ in range(args.warmup):
-        O.solve(inst, O.solver_cfg(workers=threads, time_limit=1.0))
-    # one probe run decides whether K full certifies fit in ~4 minutes
-    t0 = time.perf_counter()
-    first = O.solve(inst, cfg_full)
-    t_full = time.perf_counter() - t0
-    results = [(first.nodes_processed, t_full, first.status)]
-    budget = 240.0
-    limit = math.inf if t_full * args.steps <= budget else budget / args.steps
-    for _ in range(args.steps - 1):
+    for _ in range(args.warmup):  # untimed warm-up: bounded 1 s samples
+        O.solve(inst, O.solver_cfg(workers=threads, time_limit=min(1.0, args.time_limit)))
+    runs = []
+    for _ in range(args.steps):
         t0 = time.perf_counter()
-        c = O.solve(inst, O.solver_cfg(workers=threads, time_limit=limit))
-        results.append((c.nodes_processed, time.perf_counter() - t0, c.status))
-    nodes = sum(r[0] for r in results)
-    secs = sum(r[1] for r in results)
+        c = O.solve(inst, O.solver_cfg(workers=threads, time_limit=args.time_limit))
+        runs.append((c.nodes_processed, time.perf_counter() - t0, c))
+    nodes = sum(r[0] for r in runs)
+    secs = sum(r[1] for r in runs)
     value = nodes / secs
-    sample = (f"{args.steps} x full certify of {args.config} ({first.nodes_processed} nodes, "
-              f"{t_full:.1f} s each)" if limit == math.inf else
-              f"1 full certify ({t_full:.1f} s) + {args.steps - 1} samples capped at {limit:.0f} s")
+    c0 = runs[0][2]
+    sample = (f"{args.steps} x " + ("full certify" if math.isinf(args.time_limit)
+                                    else f"solve with a {args.time_limit:g} s limit")
+              + f" of {args.config} ({c0.nodes_processed} nodes, "
+              + ", ".join(f"{r[1]:.2f} s" for r in runs) + "); " + _cpu_desc(kind, threads, blas))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "nodes/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+        "scaling": "strong" if args.gpus > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (generate_synthetic, seed 0)",
-        "config": {"workload": f"{args.config}: {desc}, certify to 0 gap", "batch_size": "auto",
-                   "time_to_certify_s": t_full},
-        "cpu_baseline": {"value": value, "unit": "nodes/s", "cores": threads, "kind": "port",
-                         "sample": sample + ("; OpenBLAS DGEMM" if blas else "; C loops")},
+        "config": config_dict(args),
+        "result": {"status": c0.status, "time_to_certify_s": statistics.median(r[1] for r in runs)
+                   if c0.status == "optimal" else None,
+                   "nodes": c0.nodes_processed, "lb_batches": c0.lb_batches,
+                   "optimal_value": c0.optimal_value, "support": c0.support},
+        "cpu_baseline": {"value": value, "unit": "nodes/s", "cores": threads, "kind": kind,
+                         "sample": sample},
         "e2e": {"value": value, "unit": "nodes/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(spec, args):
-    from oracle import oracle as O
-    n, p, k, rho, loss, desc = spec
-    O.build()
-    threads = os.cpu_count() or 1
-    blas = O.use_openblas(threads)
+def cpu_baseline(config, time_limit):
+    """One solve of `config` by the reference on the host cores, at the same
+    time limit as the device leg (full certify when infinite)."""
+    O, kind, threads, blas = _cpu_oracle()
+    n, p, k, rho, loss, desc = CONFIGS[config]
     inst = O.generate(n, p, k, rho, loss, 5.0, 0, 2.0, 1.0)
-    limit = args.cpu_seconds
     t0 = time.perf_counter()
-    c = O.solve(inst, O.solver_cfg(workers=threads, time_limit=limit))
+    c = O.solve(inst, O.solver_cfg(workers=threads, time_limit=time_limit))
     secs = time.perf_counter() - t0
-    return {"value": c.nodes_processed / secs, "unit": "nodes/s", "cores": threads, "kind": "port",
-            "sample": (f"one certify of {args.config} on {threads} threads"
-                       + (" (OpenBLAS DGEMM)" if blas else "") +
-                       f": {c.nodes_processed} nodes in {secs:.1f} s, status {c.status}"),
+    return {"value": c.nodes_processed / secs, "unit": "nodes/s", "cores": threads, "kind": kind,
+            "sample": (f"one solve of {config}" + ("" if math.isinf(time_limit) else
+                                                   f" with a {time_limit:g} s limit")
+                       + f" by {_cpu_desc(kind, threads, blas)}: {c.nodes_processed} nodes "
+                       f"in {secs:.1f} s, status {c.status}"),
             "time_to_certify_s": secs if c.status == "optimal" else None,
-            "optimal_value": c.optimal_value, "support": c.support}
+            "optimal_value": c.optimal_value, "support": c.support,
+            "lower_bound": c.lower_bound, "gap_percent": c.gap_percent}
+
+
+ALGORITHMIC = {
+    "gemm_xv": "2*n*p flops per active column per launch",
+    "gemm_xtr": "2*n*p flops per active column per launch",
+    "pass": "4*n*p flops per node-iteration (X*V and X'*R; bound evaluations not counted)",
+    "reopt": "4*q*n flops per support-iteration of the reference's projected gradient",
+}
+
+
+def roofline(eng, certify, config, p):
+    """Dominant kernel of one extra (untimed) solve, timed per launch with CUDA
+    events on the engine stream."""
+    eng.set_timing(True)
+    before = eng.kernel_stats()
+    cert = certify(eng)
+    after = eng.kernel_stats()
+    eng.set_timing(False)
+    delta = {kc: tuple(a - b for a, b in zip(after[kc], before[kc])) for kc in after}
+    dom = max(delta, key=lambda kc: delta[kc][0])
+    ms, fl, ln = delta[dom]
+    if dom in ALGORITHMIC:
+        achieved = fl / (ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+                "peak_source": "measured FP64 DMMA issue rate (profiles/r01_fp64_peak.txt); "
+                               "MEASURED_PEAKS.json has no fp64 entry",
+                "algorithmic": ALGORITHMIC[dom]}
+    else:
+        bytes_ = 41.0 * p * cert.node_iterations if dom == "prox_fista" else float("nan")
+        achieved = bytes_ / (ms / 1e3) / 1e9
+        peak = _load_peaks().get("hbm_gbs", 6650.0)
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "algorithmic": "41*p bytes per node-iteration"}
+    roof["traffic"] = _ncu_traffic(dom, config)
+    roof["avg_launch_us"] = 1e3 * ms / max(ln, 1)
+    roof["launches"] = ln
+    roof["share_of_step"] = ms / max(1e-9, 1e3 * cert.profile.total_seconds)
+    roof["kernel_ms"] = {kc: round(v[0], 3) for kc, v in delta.items()}
+    return roof
+
+
+def secondary(P, torch, flush, local, args):
+    """c3 / c4 at stated time limits: device nodes/s with clocks and roofline,
+    and the reference on the host cores at the same limit."""
+    out = {}
+    for name, limit in (("c3", args.c3_limit), ("c4", args.c4_limit)):
+        n, p, k, rho, loss, desc = CONFIGS[name]
+        inst, _ = P.generate_synthetic(P.GeneratorSpec(n=n, p=p, k=k, correlation=rho, loss=loss,
+                                                       seed=0, M=2.0, lambda2=1.0))
+        eng = P.Engine(inst, device=local)
+        warm = P.SolverConfig(time_limit=min(2.0, limit))
+        eng.solve(warm)  # untimed warm-up
+        cfg = P.SolverConfig(time_limit=limit)
+        flush.zero_()
+        torch.cuda.synchronize()
+        sampler = ClockSampler(local)
+        sampler.start()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        cert = eng.solve(cfg)
+        e1.record()
+        torch.cuda.synchronize()
+        clocks = sampler.stop()
+        secs = e0.elapsed_time(e1) / 1e3
+        roof = roofline(eng, lambda e: e.solve(P.SolverConfig(time_limit=min(5.0, limit))),
+                        name, p)
+        eng.close()
+        entry = {"workload": f"{name}: {desc}, nodes/s within a {limit:g} s time limit",
+                 "value": cert.nodes_processed / secs, "unit": "nodes/s", "seconds": secs,
+                 "nodes": cert.nodes_processed, "lb_batches": cert.lb_batches,
+                 "status": cert.status, "optimal_value": cert.optimal_value,
+                 "support": cert.support, "lower_bound": cert.lower_bound,
+                 "gap_percent": cert.gap_percent, "clocks": clocks,
+                 "roofline": {k2: v for k2, v in roof.items() if k2 != "kernel_ms"} |
+                             {"kernel_ms": roof["kernel_ms"],
+                              "measured_on": "one solve with a 5 s limit"}}
+        if not args.no_cpu_baseline:
+            entry["cpu_baseline"] = cpu_baseline(name, limit)
+        out[name] = entry
+    return out
 
 
 def main():
@@ -203,25 +326,32 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="default: c2 at one GPU, c4 (certify) for N > 1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=120.0)
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the c3/c4 secondary block (N = 1)")
+    ap.add_argument("--c3-limit", type=float, default=20.0)
+    ap.add_argument("--c4-limit", type=float, default=30.0)
     ap.add_argument("--cpu-baseline-only", action="store_true",
-                    help="only the cpu_baseline leg for --config (bounded by --cpu-seconds)")
+                    help="only the cpu_baseline leg for --config at --time-limit")
     ap.add_argument("--time-limit", type=float, default=float("inf"),
-                    help="per-certify time limit (c3/c4: nodes/s at a stated limit)")
+                    help="per-solve time limit (c3/c4: nodes/s at a stated limit)")
     args = ap.parse_args()
-    spec = CONFIGS[args.config]
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local = _env_int("LOCAL_RANK", 0)
+    if args.config is None:
+        args.config = "c2" if max(world, args.gpus) == 1 else "c4"
+    spec = CONFIGS[args.config]
 
     if args.impl == "reference":
         run_reference(args, spec, rank)
         return
     if args.cpu_baseline_only:
         if rank == 0:
-            print(json.dumps({"config": args.config, "cpu_baseline": cpu_baseline(spec, args)}),
+            print(json.dumps({"config": args.config,
+                              "cpu_baseline": cpu_baseline(args.config, args.time_limit)}),
                   flush=True)
         return
 
@@ -243,13 +373,17 @@ def main():
     eng = P.Engine(inst, device=local)  # X, y resident in HBM before timing
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > L2
 
-    def certify(engine):
+    def certify(engine, c=cfg):
         if args.config == "c5":  # collect_rashomon (rashomon.hpp:149-218): same hot path
-            return engine.collect_rashomon(cfg, P.RashomonConfig(epsilon=0.01)).certificate
-        return engine.solve_sharded(cfg, transport="nccl") if sharded else engine.solve(cfg)
+            return engine.collect_rashomon(c, P.RashomonConfig(epsilon=0.01)).certificate
+        return engine.solve_sharded(c, transport="nccl") if sharded else engine.solve(c)
 
+    # warm-up: full solves for the fast configs; c3/c4 warm up on short
+    # time-limited solves (they exercise every kernel; a full c4 certify is ~50 s)
+    warm_cfg = cfg if args.config in ("c1", "c2", "c5") else \
+        P.SolverConfig(time_limit=min(3.0, args.time_limit))
     for _ in range(args.warmup):
-        certify(eng)
+        certify(eng, warm_cfg)
 
     def barrier():
         torch.cuda.synchronize()
@@ -285,55 +419,22 @@ def main():
     total_ms_max, nodes_all = float(t[0]), float(nodes)
     value = nodes_all / (total_ms_max / 1e3)
 
-    # roofline: one extra (untimed) certify with per-launch CUDA events on the engine stream
-    eng.set_timing(True)
-    before = eng.kernel_stats()
-    prof_cert = certify(eng)
-    after = eng.kernel_stats()
-    eng.set_timing(False)
-    delta = {kc: tuple(a - b for a, b in zip(after[kc], before[kc])) for kc in after}
-    dom = max(delta, key=lambda kc: delta[kc][0])
-    ms, fl, ln = delta[dom]
-    peaks = _load_peaks()
-    algorithmic = {
-        "gemm_xv": "2*n*p flops per active column per launch",
-        "gemm_xtr": "2*n*p flops per active column per launch",
-        "pass": "4*n*p flops per node-iteration (X*V and X'*R; bound evaluations not counted)",
-        "reopt": "4*q*n flops per support-iteration of the reference's projected gradient",
-    }
-    if dom in algorithmic:
-        achieved = fl / (ms / 1e3) / 1e12
-        roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
-                "peak_source": "measured FP64 DMMA issue rate (profiles/r01_fp64_peak.txt); "
-                               "MEASURED_PEAKS.json has no fp64 entry",
-                "algorithmic": algorithmic[dom]}
-    else:
-        node_its = prof_cert.node_iterations
-        bytes_ = 41.0 * p * node_its if dom == "prox_fista" else float("nan")
-        achieved = bytes_ / (ms / 1e3) / 1e9
-        peak = peaks.get("hbm_gbs", 6650.0)
-        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                "algorithmic": "41*p bytes per node-iteration"}
-    roof["traffic"] = _ncu_traffic(dom, args.config)
-    roof["avg_launch_us"] = 1e3 * ms / max(ln, 1)
-    roof["share_of_step"] = ms / max(1e-9, 1e3 * prof_cert.profile.total_seconds)
-    roof["kernel_ms"] = {kc: round(v[0], 3) for kc, v in delta.items()}
+    roof = roofline(eng, certify, args.config, p)
 
     # e2e: the public API from host arrays (instance upload, solve, certificate readback)
     e2e_ms, e2e_nodes, h2d, d2h = 0.0, 0, 0, 0
     e2e_parts = [0.0, 0.0, 0.0]  # create (upload + L), solve, destroy
     # W untimed warm-up rounds first, as for the device-timed steps (the first
     # create of a process grows the stream-ordered memory pool)
-    for it in range(args.warmup + args.steps):
-        timed = it >= args.warmup
+    e2e_warm = args.warmup if args.config in ("c1", "c2", "c5") else 1
+    for it in range(e2e_warm + args.steps):
+        timed = it >= e2e_warm
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         e2 = P.Engine(inst, device=local)
         t1 = time.perf_counter()
-        c2 = certify(e2)
+        c2 = certify(e2, cfg if timed else warm_cfg)
         bi, bo = e2.transfer_bytes()
         t2 = time.perf_counter()
         e2.close()
@@ -354,9 +455,14 @@ def main():
         e2e_ms = float(te[0])
     e2e_value = e2e_nodes / (e2e_ms / 1e3)
 
+    sec = None
+    if rank == 0 and world == 1 and not args.no_secondary and args.config in ("c1", "c2", "c5"):
+        eng.close()
+        sec = secondary(P, torch, flush, local, args)
+
     base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        base = cpu_baseline(spec, args)
+        base = cpu_baseline(args.config, args.time_limit)
         if base.get("support") is not None and base["support"] != certs[0].support:
             base["support_mismatch"] = True
 
@@ -368,15 +474,12 @@ def main():
             "higher_is_better": True, "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (generate_synthetic, seed 0, problem.hpp:70-132)",
-            "config": {"workload": f"{args.config}: {desc}, " + (
-                           "certify to 0 gap" if math.isinf(args.time_limit)
-                           else f"nodes/s within a {args.time_limit:g} s time limit"),
-                       "n": n, "p": p, "k": k, "rho": rho, "loss": "logistic" if loss else "squared",
+            "config": config_dict(args),
+            "parallelism": f"node-sharded over {world} GPUs (NCCL)" if sharded else "single GPU",
+            "result": {"status": c0.status,
+                       "time_to_certify_s": total_ms_max / args.steps / 1e3
+                       if c0.status == "optimal" else None,
                        "batch_size": c0.batch_size_used,
-                       "parallelism": f"node-sharded over {world} GPUs (NCCL)" if sharded
-                       else "single GPU",
-                       "l2": "flushed (256 MiB write) before every step",
-                       "time_to_certify_s": total_ms_max / args.steps / 1e3,
                        "nodes_per_certify": c0.nodes_processed, "lb_batches": c0.lb_batches,
                        "relax_iterations": c0.relax_iterations,
                        "node_iterations": c0.node_iterations,
@@ -393,6 +496,7 @@ def main():
                     "time_to_certify_s": e2e_ms / args.steps / 1e3,
                     "create_solve_destroy_s": [round(x / args.steps, 5) for x in e2e_parts]},
             "cpu_baseline": base,
+            "secondary": sec,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -18,7 +18,11 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "_build", "liboracle.so")
-_lib = None
+# The reference itself (its headers compiled through the Eigen-subset shim,
+# oracle/ref/), exporting the same orc_* C API: backend "ref".
+REF_LIB_PATH = os.path.join(_HERE, "_ref", "libbnbref.so")
+_libs = {}
+_backend = "c"
 
 SQUARED, LOGISTIC = 0, 1
 FREE, ONE, ZERO = 0, 1, 2
@@ -26,9 +30,43 @@ PRUNABLE, CONVERGED, CAPPED = 0, 1, 2
 
 
 def build() -> str:
-    """Compile the oracle (gcc, seconds)."""
+    """Compile the oracle (gcc, seconds) and, where /root/reference exists,
+    the reference itself into oracle/_ref (g++, ~15 s)."""
     subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    subprocess.run(["make", "-s", "-C", os.path.join(_HERE, "ref")], check=True)
     return _LIB_PATH
+
+
+def ref_available() -> bool:
+    """True when oracle/_ref/libbnbref.so (the compiled reference) exists."""
+    return os.path.exists(REF_LIB_PATH)
+
+
+def set_backend(name: str) -> str:
+    """Select which library answers every call: "c" (oracle.c, the
+    restatement) or "ref" (the reference headers compiled via the shim).
+    Returns the previous backend."""
+    global _backend
+    if name not in ("c", "ref"):
+        raise ValueError(name)
+    if name == "ref" and not ref_available():
+        raise FileNotFoundError(REF_LIB_PATH)
+    prev, _backend = _backend, name
+    return prev
+
+
+class backend:
+    """Context manager: ``with backend("ref"): ...``"""
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        self.prev = set_backend(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        set_backend(self.prev)
 
 
 class RelaxCfg(C.Structure):
@@ -65,11 +103,11 @@ _up = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
 
 
 def lib():
-    global _lib
-    if _lib is None:
-        if not os.path.exists(_LIB_PATH):
+    if _backend not in _libs:
+        path = _LIB_PATH if _backend == "c" else REF_LIB_PATH
+        if not os.path.exists(path):
             build()
-        L = C.CDLL(_LIB_PATH)
+        L = C.CDLL(path)
         d, i, u64, vp = C.c_double, C.c_int, C.c_uint64, C.c_void_p
         L.orc_loss_value.restype = d
         L.orc_loss_value.argtypes = [i, d, d]
@@ -111,8 +149,8 @@ def lib():
         L.orc_pool_record.argtypes = [vp, i, _ip, _dp, C.POINTER(d)]
         L.orc_pool_free.argtypes = [vp]
         L.orc_use_openblas.argtypes = [C.c_char_p, i]
-        _lib = L
-    return _lib
+        _libs[_backend] = L
+    return _libs[_backend]
 
 
 def use_openblas(threads: int = 0) -> bool:
@@ -176,12 +214,21 @@ class Instance:
         return np.asfortranarray(self.X).ravel(order="F")
 
 
-def generate(n, p, k, rho, loss, snr=5.0, seed=0, M=2.0, lambda2=1.0) -> Instance:
-    """problem.hpp:70-132 generate_synthetic."""
+def generate(n, p, k, rho, loss, snr=5.0, seed=0, M=2.0, lambda2=1.0,
+             reference_generator=False) -> Instance:
+    """problem.hpp:70-132 generate_synthetic.
+
+    The instance fixture is always oracle.c's restatement (AR(1) Cholesky
+    factor in closed form), whose bytes equal the product's generator
+    (tests/test_io_cpu.py), whatever the backend: every leg then sees the
+    same X, y.  reference_generator=True runs the reference's own
+    generate_synthetic (oracle/_ref; LLT through the shim), which agrees to
+    rounding (tests/test_ref_cpu.py)."""
     X = np.zeros(n * p, dtype=np.float64)
     y = np.zeros(n, dtype=np.float64)
     sup = np.zeros(k, dtype=np.int32)
-    rc = lib().orc_generate(n, p, k, rho, loss, snr, seed, X, y, sup)
+    with backend("ref" if reference_generator else "c"):
+        rc = lib().orc_generate(n, p, k, rho, loss, snr, seed, X, y, sup)
     if rc != 0:
         raise ValueError("generator: invalid spec")
     return Instance(X.reshape(p, n).T, y, loss, k, M, lambda2, sup.tolist())

@@ -191,7 +191,7 @@ bnbg::RelaxParams relax_params(const bnbg_relax_cfg& c) {
 // Incumbent record exchanged between ranks: objective, |support|, support
 // (sorted) and coefficients, as doubles.
 struct IncRecord {
-  static size_t doubles(int k) { return 2 + 2 * (size_t)k; }
+  static size_t doubles(int k) { return 3 + 2 * (size_t)k; }  // + the pass's error code
 };
 
 // bnb_engine.hpp:116-291 run_bnb.  With `comm` the nodes are sharded over
@@ -246,6 +246,30 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
   std::vector<int> batch_slots, n01, j0s, j1s, child_slots, rec;
   std::vector<double> batch_lb, rec_lb;
   const int kk = std::max(k, 1);
+  // Sharded: a rank whose pass fails keeps taking part in the pass's
+  // collectives with its error code, so every rank leaves together with a
+  // non-OK status instead of blocking in the next allgather.
+  int pass_rc = 0;
+  std::string pass_msg;
+  auto fail = [&](int rc, const std::string& msg) -> int {
+    if (!comm) return set_err(h, rc, msg);
+    if (!pass_rc) {
+      pass_rc = rc;
+      pass_msg = msg;
+    }
+    return 0;
+  };
+  // After a collective: the lowest-ranked failure ends the solve on all ranks.
+  auto collective_error = [&](const double* codes, size_t stride) -> int {
+    for (int r = 0; r < world; ++r) {
+      const int rc = (int)codes[(size_t)r * stride];
+      if (!rc) continue;
+      if (r == rank) return set_err(h, rc, pass_msg);
+      return set_err(h, rc, "sharded solve: rank " + std::to_string(r) + " failed (code " +
+                                std::to_string(rc) + ")");
+    }
+    return 0;
+  };
 
   while (comm ? global_open > 0 : (!queue.empty() || !pending.empty())) {
     if (comm ? global_stop : elapsed() > cfg.time_limit) {
@@ -285,7 +309,11 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
       Timer t(cert->lower_bound_seconds);
       const int rc = eng.relax_pool(m, batch_slots.data(), rp, threshold, on_dual != nullptr, pr,
                                     on_dual != nullptr, &n01, &j0s, &j1s);
-      if (rc) return set_err(h, rc, eng.err);
+      if (rc) {
+        if (int e = fail(rc, eng.err)) return e;
+      }
+    }
+    if (m > 0 && !pass_rc) {
       ++cert->lb_batches;
       cert->relax_iterations += pr.iterations;
       cert->node_iterations += pr.node_iterations;
@@ -308,7 +336,7 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
         sidx.insert(sidx.end(), leaf.j1.begin(), leaf.j1.end());
         offsets.push_back((int)sidx.size());
       }
-      for (int b = 0; b < m; ++b) {
+      for (int b = 0; b < m && !pass_rc; ++b) {
         if (pr.status[b] == BNBG_PRUNABLE) continue;
         const int* row = pr.sup.data() + (size_t)b * kk;
         sidx.insert(sidx.end(), row, row + pr.len[b]);
@@ -317,16 +345,20 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
     }
     const int nsup = (int)offsets.size() - 1;
     std::vector<double> coef(sidx.size() + 1), obj(nsup + 1);
-    if (nsup > 0) {
+    if (nsup > 0 && !pass_rc) {
       Timer t(cert->reoptimization_seconds);
       const int rc = eng.reoptimize(nsup, offsets.data(), sidx.data(), coef.data(), obj.data());
-      if (rc) return set_err(h, rc, eng.err);
+      if (rc) {
+        if (int e = fail(rc, eng.err)) return e;
+      }
+    }
+    if (nsup > 0 && !pass_rc) {
       ++cert->reopt_batches;
       cert->reopt_supports += nsup;
     }
     {
       Timer t(cert->branch_generate_seconds);
-      for (int s = 0; s < nsup; ++s) {  // incumbent update (bnb_engine.hpp:216-240)
+      for (int s = 0; s < nsup && !pass_rc; ++s) {  // incumbent update (bnb_engine.hpp:216-240)
         const int len = offsets[s + 1] - offsets[s];
         const int* sq = sidx.data() + offsets[s];
         const double* cf = coef.data() + offsets[s];
@@ -347,6 +379,7 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
       if (comm) {  // global incumbent: lowest objective, ties to the lowest rank
         const size_t R = IncRecord::doubles(kk);
         std::vector<double> mine(R, 0.0), all(R * world);
+        mine[R - 1] = (double)pass_rc;  // error code of this rank's pass
         mine[0] = inc_obj;
         mine[1] = (double)inc_sup.size();
         for (size_t i = 0; i < inc_sup.size(); ++i) {
@@ -355,6 +388,7 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
         }
         if (int rc = comm->allgather(eng, mine.data(), sizeof(double) * R, all.data()))
           return set_err(h, rc, eng.err);
+        if (int e = collective_error(all.data() + R - 1, R)) return e;
         int win = -1;
         for (int r = 0; r < world; ++r)
           if (win < 0 || all[R * r] < all[R * win]) win = r;
@@ -375,13 +409,19 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
         // prune test, branch variable and children on the device (:243-256)
         child_slots.resize(2 * (size_t)m);
         for (int i = 0; i < 2 * m; ++i) child_slots[i] = slots.take();
-        if (int rc = eng.pool_reserve(slots.high_water())) return set_err(h, rc, eng.err);
         int surv = 0, bad = -1;
-        const int rc = eng.branch_pool(m, batch_slots.data(), batch_lb.data(), post_threshold,
-                                       child_slots.data(), surv, bad, rec, rec_lb);
-        if (rc) return set_err(h, rc, eng.err);
-        if (bad >= 0)
-          return set_err(h, BNBG_LOGIC_ERROR, "select_branch_variable: no free coordinate");
+        int rc = eng.pool_reserve(slots.high_water());
+        if (!rc)
+          rc = eng.branch_pool(m, batch_slots.data(), batch_lb.data(), post_threshold,
+                               child_slots.data(), surv, bad, rec, rec_lb);
+        if (rc) {
+          if (int e = fail(rc, eng.err)) return e;
+          surv = 0;
+        } else if (bad >= 0) {
+          if (int e = fail(BNBG_LOGIC_ERROR, "select_branch_variable: no free coordinate"))
+            return e;
+          surv = 0;
+        }
         for (int i = 2 * m - 1; i >= 2 * surv; --i) slots.give(child_slots[i]);
         const int RI = 4 + kk;
         for (int c = 0; c < 2 * surv; ++c) {
@@ -400,18 +440,19 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
       Timer t(cert->transfer_seconds);
       double lb_local = queue.global_lb();
       for (const Leaf& leaf : pending) lb_local = std::min(lb_local, leaf.lb);
-      const double mine[4] = {(double)queue.size(), (double)pending.size(), lb_local,
-                              elapsed() > cfg.time_limit ? 1.0 : 0.0};
-      std::vector<double> all(4 * (size_t)world);
+      const double mine[5] = {(double)queue.size(), (double)pending.size(), lb_local,
+                              elapsed() > cfg.time_limit ? 1.0 : 0.0, (double)pass_rc};
+      std::vector<double> all(5 * (size_t)world);
       if (int rc = comm->allgather(eng, mine, sizeof(mine), all.data()))
         return set_err(h, rc, eng.err);
+      if (int e = collective_error(all.data() + 4, 5)) return e;
       global_open = 0;
       global_stop = false;
       std::vector<int64_t> counts(world), moves((size_t)world * world);
       for (int r = 0; r < world; ++r) {
-        counts[r] = (int64_t)all[4 * r];
-        global_open += counts[r] + (int64_t)all[4 * r + 1];
-        global_stop = global_stop || all[4 * r + 3] != 0.0;
+        counts[r] = (int64_t)all[5 * r];
+        global_open += counts[r] + (int64_t)all[5 * r + 1];
+        global_stop = global_stop || all[5 * r + 3] != 0.0;
       }
       if (global_open > 0 && !global_stop &&
           bnbg::balance_plan(world, counts.data(), moves.data())) {
@@ -517,6 +558,20 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
 // ===========================================================================
 // C-ABI
 // ===========================================================================
+extern "C" {
+
+}  // extern "C" (helper below is internal)
+
+// The pool pass seam is two calls (bnbg_pool_relax, then bnbg_pool_branch)
+// sharing the batch workspaces (slots, states, betas, status, best bounds,
+// branch variables).  Every other entry point that may write those buffers
+// or the pool ends the pass: a later bnbg_pool_branch is rejected instead of
+// branching on overwritten data.
+static void end_pool_pass(bnbg_handle* h) {
+  h->last_pool_m = 0;
+  h->last_pool_slots.clear();
+}
+
 extern "C" {
 
 void bnbg_relax_cfg_default(bnbg_relax_cfg* c) {
@@ -650,6 +705,7 @@ int bnbg_relax_batch(bnbg_handle* h, const bnbg_relax_cfg* cfg, int m, const uin
                      const int32_t* kbar, const double* warm, double prune_threshold,
                      double* beta_out, double* bounds_out, int32_t* status_out,
                      int32_t* iters_out, bnbg_trace_fn trace, void* user) {
+  end_pool_pass(h);
   bnbg_relax_cfg c;
   if (cfg)
     c = *cfg;
@@ -682,6 +738,7 @@ int bnbg_relax_batch(bnbg_handle* h, const bnbg_relax_cfg* cfg, int m, const uin
 int bnbg_round_support(bnbg_handle* h, int m, const double* beta, const uint8_t* state,
                        const int32_t* kbar, const int32_t* one_off, const int32_t* one_idx,
                        int32_t* support_out, int32_t* len_out) {
+  end_pool_pass(h);
   const int rc = h->eng.round_select(m, beta, state, kbar, one_off, one_idx, support_out, len_out,
                                      nullptr);
   return rc ? set_err(h, rc, h->eng.err) : BNBG_OK;
@@ -689,6 +746,7 @@ int bnbg_round_support(bnbg_handle* h, int m, const double* beta, const uint8_t*
 
 int bnbg_select_branch(bnbg_handle* h, int m, const double* beta, const uint8_t* state,
                        int32_t* j_out) {
+  end_pool_pass(h);
   std::vector<int> kb(std::max(m, 1), 0);
   const int rc =
       h->eng.round_select(m, beta, state, kb.data(), nullptr, nullptr, nullptr, nullptr, j_out);
@@ -706,6 +764,7 @@ int bnbg_reoptimize(bnbg_handle* h, int nsup, const int32_t* offsets, const int3
 }
 
 int bnbg_pool_root(bnbg_handle* h, int slot) {
+  end_pool_pass(h);
   if (slot < 0) return set_err(h, BNBG_INPUT_ERROR, "pool_root: slot must be nonnegative");
   const int rc = h->eng.pool_root(slot);
   return rc ? set_err(h, rc, h->eng.err) : BNBG_OK;
@@ -749,9 +808,18 @@ int bnbg_pool_branch(bnbg_handle* h, int m, const double* lb_in, double post_thr
                      double* child_lb_out) {
   if (m != h->last_pool_m || m <= 0)
     return set_err(h, BNBG_INPUT_ERROR, "pool_branch: m must match the last pool_relax batch");
-  for (int i = 0; i < 2 * m; ++i)
-    if (free_slots[i] < 0)
+  {
+    // children are written while the parents' pool slots are read: the 2m
+    // free slots must be distinct and disjoint from the batch's slots
+    std::vector<int> seen(free_slots, free_slots + 2 * m);
+    seen.insert(seen.end(), h->last_pool_slots.begin(), h->last_pool_slots.end());
+    std::sort(seen.begin(), seen.end());
+    if (!seen.empty() && seen.front() < 0)
       return set_err(h, BNBG_INPUT_ERROR, "pool_branch: free slots must be nonnegative");
+    if (std::adjacent_find(seen.begin(), seen.end()) != seen.end())
+      return set_err(h, BNBG_INPUT_ERROR,
+                     "pool_branch: free slots must be distinct and not slots of the batch");
+  }
   int hw = 0;
   for (int i = 0; i < 2 * m; ++i) hw = std::max(hw, free_slots[i] + 1);
   if (int rc = h->eng.pool_reserve(hw)) return set_err(h, rc, h->eng.err);
@@ -760,6 +828,7 @@ int bnbg_pool_branch(bnbg_handle* h, int m, const double* lb_in, double post_thr
   std::vector<double> rlb;
   const int rc = h->eng.branch_pool(m, h->last_pool_slots.data(), lb_in, post_threshold,
                                     free_slots, surv, bad, rec, rlb);
+  end_pool_pass(h);  // one branch per relaxed batch
   if (rc) return set_err(h, rc, h->eng.err);
   if (bad >= 0) return set_err(h, BNBG_LOGIC_ERROR, "select_branch_variable: no free coordinate");
   *survivors_out = surv;
@@ -769,12 +838,14 @@ int bnbg_pool_branch(bnbg_handle* h, int m, const double* lb_in, double post_thr
 }
 
 int bnbg_gemm(bnbg_handle* h, int trans, int m, const double* B, double* C) {
+  end_pool_pass(h);
   const int rc = h->eng.gemm_probe(trans, m, B, C);
   return rc ? set_err(h, rc, h->eng.err) : BNBG_OK;
 }
 
 int bnbg_solve(bnbg_handle* h, const bnbg_solver_cfg* cfg, bnbg_certificate* cert,
                bnbg_dual_hook on_dual, bnbg_boundary_hook on_boundary, void* user) {
+  end_pool_pass(h);
   bnbg_solver_cfg c;
   if (cfg)
     c = *cfg;
@@ -798,6 +869,7 @@ int bnbg_nccl_init(bnbg_handle* h, const uint8_t* uid, int rank, int world) {
 
 int bnbg_solve_sharded(bnbg_handle* h, const bnbg_solver_cfg* cfg, const bnbg_comm_ops* ops,
                        bnbg_certificate* cert) {
+  end_pool_pass(h);
   bnbg_solver_cfg c;
   if (cfg)
     c = *cfg;
@@ -829,6 +901,7 @@ int bnbg_solve_sharded(bnbg_handle* h, const bnbg_solver_cfg* cfg, const bnbg_co
 
 int bnbg_collect_rashomon(bnbg_handle* h, const bnbg_solver_cfg* cfg, double epsilon, long long cap,
                           bnbg_certificate* cert, bnbg_pool** pool_out) {
+  end_pool_pass(h);
   *pool_out = nullptr;
   if (epsilon < 0.0) return set_err(h, BNBG_INPUT_ERROR, "rashomon: epsilon must be nonnegative");
   bnbg_solver_cfg c;

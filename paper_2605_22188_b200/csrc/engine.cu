@@ -33,7 +33,8 @@ static int* pinned_slot_acquire() {
     }
   }
   void* p = nullptr;
-  if (cudaMallocHost(&p, 64) != cudaSuccess) return nullptr;
+  // portable: a released slot may be reused by an engine on another device
+  if (cudaHostAlloc(&p, 64, cudaHostAllocPortable) != cudaSuccess) return nullptr;
   return static_cast<int*>(p);
 }
 
@@ -102,6 +103,9 @@ Engine::~Engine() {
   dfree(dOneLen_);
   dfree(dOneIdx_);
   dfree(dLists_);
+  // an error path may have left a d2h copy into hPin_ in flight: drain the
+  // stream before the slot returns to the process-wide free list
+  if (stream_) cudaStreamSynchronize(stream_);
   if (hPin_) pinned_slot_release(hPin_);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);

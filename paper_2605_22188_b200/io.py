@@ -177,9 +177,23 @@ def certificate_to_json(cert, include_profile: bool = False) -> dict:
     return out
 
 
+def _finite_or_null(obj):
+    """nlohmann::json writes non-finite doubles as null (e.g. optimal_value of
+    a time-limited run with no incumbent, lower_bound of an unprocessed root)."""
+    if isinstance(obj, float):
+        return obj if math.isfinite(obj) else None
+    if isinstance(obj, dict):
+        return {k: _finite_or_null(v) for k, v in obj.items()}
+    if isinstance(obj, (list, tuple)):
+        return [_finite_or_null(v) for v in obj]
+    return obj
+
+
 def dump_json(obj) -> str:
-    """nlohmann::json::dump() layout: keys sorted, no whitespace."""
-    return json.dumps(obj, sort_keys=True, separators=(",", ":"))
+    """nlohmann::json::dump() layout: keys sorted, no whitespace, non-finite
+    numbers as null (allow_nan=False catches any that slip through)."""
+    return json.dumps(_finite_or_null(obj), sort_keys=True, separators=(",", ":"),
+                      allow_nan=False)
 
 
 def fnv1a(data: bytes) -> int:

@@ -26,3 +26,21 @@ def bnb():
     import paper_2605_22188_b200 as P
     P._L.lib()
     return P
+
+
+def _ref_params():
+    from oracle import oracle as O
+    return ["c", "ref"] if (O.ref_available() or os.path.isdir("/root/reference")) else ["c"]
+
+
+@pytest.fixture(params=_ref_params())
+def orc_any(request, orc):
+    """The checker under both backends: "c" = oracle.c (the restatement),
+    "ref" = the reference itself (oracle/_ref/libbnbref.so, its headers
+    compiled through the Eigen-subset shim).  Running the oracle's pinning
+    tests on both pins the restatement to the reference."""
+    prev = orc.set_backend(request.param)
+    try:
+        yield orc
+    finally:
+        orc.set_backend(prev)

@@ -88,3 +88,17 @@ def test_fnv1a_fingerprint(tmp_path):
     path = tmp_path / "f.bin"
     path.write_bytes(b"foobar")
     assert bio.file_fingerprint(str(path)) == 0x85944171f73967e8
+
+
+def test_certificate_json_time_limit_zero(bnb):
+    """A time_limit=0 certificate (no incumbent, root unprocessed): nlohmann
+    writes the non-finite optimal_value / lower_bound as null."""
+    cert = bnb.Certificate(optimal_value=math.inf, support=[], coefficients=np.array([]),
+                           gap_percent=100.0, lower_bound=-math.inf, nodes_processed=0,
+                           lb_batches=0, reopt_batches=0, batch_size_used=8192,
+                           profile=bnb.ComponentProfile(0.0, 0.0, 0.0, 0.0, 0.0),
+                           status="time_limit")
+    s = bio.dump_json(bio.certificate_to_json(cert))
+    d = json.loads(s)
+    assert d["optimal_value"] is None and d["lower_bound"] is None
+    assert "Infinity" not in s and "NaN" not in s

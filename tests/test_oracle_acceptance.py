@@ -17,9 +17,9 @@ def _enum_cases():
         return json.load(f)
 
 
-def test_acceptance1_exactness_vs_enumeration(orc):
+def test_acceptance1_exactness_vs_enumeration(orc_any):
     """#1: 50 seeded instances per loss, value within 1e-6, gap 0."""
-    O = orc
+    O = orc_any
     for case in _enum_cases():
         inst = O.generate(30, 12, 3, 0.9, case["loss"], 5.0, case["seed"], 2.0, 1.0)
         assert fnv1a(inst.xflat(), inst.y) == case["fingerprint"]
@@ -29,9 +29,9 @@ def test_acceptance1_exactness_vs_enumeration(orc):
         assert cert.support == case["support"]
 
 
-def test_acceptance2_safe_bounds(orc):
+def test_acceptance2_safe_bounds(orc_any):
     """#2: every traced dual bound <= the node's true optimum."""
-    O = orc
+    O = orc_any
     total = 0
     for loss in (O.SQUARED, O.LOGISTIC):
         for seed in range(4):
@@ -56,9 +56,9 @@ def test_acceptance2_safe_bounds(orc):
     assert total > 500
 
 
-def test_acceptance6_rashomon_completeness(orc):
+def test_acceptance6_rashomon_completeness(orc_any):
     """#6: pool == enumerated epsilon-Rashomon set (size-k supports), and cap N=5."""
-    O = orc
+    O = orc_any
     eps = 0.1
     for loss in (O.SQUARED, O.LOGISTIC):
         for seed in range(3):
@@ -81,8 +81,8 @@ def test_acceptance6_rashomon_completeness(orc):
             np.testing.assert_allclose(sorted(o for _, _, o in pool5), best5, rtol=1e-6)
 
 
-def test_acceptance11_determinism_across_workers(orc):
-    O = orc
+def test_acceptance11_determinism_across_workers(orc_any):
+    O = orc_any
     inst = O.generate(200, 40, 4, 0.8, O.LOGISTIC, 5.0, 7, 2.0, 1.0)
     a = O.solve(inst, O.solver_cfg(workers=1))
     b = O.solve(inst, O.solver_cfg(workers=4))

@@ -9,8 +9,8 @@ import numpy as np
 import pytest
 
 
-def test_losses_known_answers(orc):
-    O = orc
+def test_losses_known_answers(orc_any):
+    O = orc_any
     assert O.loss_value(O.SQUARED, 3.0, 3.0) == 0.0
     assert abs(O.loss_value(O.LOGISTIC, 0.0, 1.0) - math.log(2)) < 1e-12
     assert abs(O.loss_value(O.LOGISTIC, 2.0, -1.0) - 2.126928) < 1e-6
@@ -26,8 +26,8 @@ def test_losses_known_answers(orc):
         assert math.isfinite(O.loss_derivative(O.LOGISTIC, s, -1.0))
 
 
-def test_fenchel_young_and_finite_differences(orc):
-    O = orc
+def test_fenchel_young_and_finite_differences(orc_any):
+    O = orc_any
     rng = np.random.default_rng(1)
     for loss in (O.SQUARED, O.LOGISTIC):
         for _ in range(2000):
@@ -41,8 +41,8 @@ def test_fenchel_young_and_finite_differences(orc):
             assert abs(fd - z) <= 1e-6 * max(1.0, abs(z))
 
 
-def test_smoothness_known_answers(orc):
-    O = orc
+def test_smoothness_known_answers(orc_any):
+    O = orc_any
     assert abs(O.smoothness(O.SQUARED, np.eye(2)) - 1.01) < 1e-12
     assert abs(O.smoothness(O.LOGISTIC, np.diag([3.0])) - 1.01 * 9 / 4) < 1e-12
     rng = np.random.default_rng(2)
@@ -52,8 +52,8 @@ def test_smoothness_known_answers(orc):
     assert O.smoothness(O.SQUARED, np.zeros((3, 2))) == 1e-12                # losses.hpp:103
 
 
-def test_prox_known_answers(orc):
-    O = orc
+def test_prox_known_answers(orc_any):
+    O = orc_any
     assert O.prox_huber(3.0, 0.0, 2.0) == 3.0
     assert O.prox_huber(1.0, 1.0, 2.0) == 0.5
     assert O.prox_huber(10.0, 1.0, 2.0) == 8.0
@@ -66,8 +66,8 @@ def test_prox_known_answers(orc):
     assert np.all(O.prox_step_column(np.ones(4), st, 4, 3.0, 2.0) == 0)
 
 
-def test_g_and_recovery_known_answers(orc):
-    O = orc
+def test_g_and_recovery_known_answers(orc_any):
+    O = orc_any
     assert O.g_value(np.zeros(4), None, 2, 2.0) == 0.0
     assert abs(O.g_value([2, 1, 0.5, 0.25], None, 2, 2.0) - 3.53125) < 1e-12
     st = np.array([O.ONE, O.FREE, O.FREE], dtype=np.uint8)
@@ -79,9 +79,9 @@ def test_g_and_recovery_known_answers(orc):
     assert O.select_branch([0.1, -3.0, 0.2], None) == 1                      # SPEC.md:325 (1-based 2)
 
 
-def test_boundary_seeded_pava_equals_generic(orc):
+def test_boundary_seeded_pava_equals_generic(orc_any):
     """boundary-seeded PAVA == generic full-scan PAVA."""
-    O = orc
+    O = orc_any
     rng = np.random.default_rng(3)
     for _ in range(400):
         p = int(rng.integers(2, 40))
@@ -95,9 +95,9 @@ def test_boundary_seeded_pava_equals_generic(orc):
         np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-12)
 
 
-def test_prox_step_feasible_and_optimal(orc):
+def test_prox_step_feasible_and_optimal(orc_any):
     """SPEC.md:136 feasibility and the variational inequality of SPEC.md:165."""
-    O = orc
+    O = orc_any
     rng = np.random.default_rng(4)
     for _ in range(60):
         p = int(rng.integers(3, 9))
@@ -126,8 +126,8 @@ def test_prox_step_feasible_and_optimal(orc):
                 assert f1 >= f0 - 1e-8
 
 
-def test_generator_and_auto_batch(orc):
-    O = orc
+def test_generator_and_auto_batch(orc_any):
+    O = orc_any
     inst = O.generate(1000, 100, 5, 0.5, O.SQUARED)
     assert inst.support == [19, 39, 59, 79, 99]                              # problem.hpp:101-107
     inst2 = O.generate(1000, 100, 5, 0.5, O.SQUARED)
@@ -145,9 +145,9 @@ def test_generator_and_auto_batch(orc):
     assert O.auto_batch_size(10, 100, 100, 5, O.SQUARED) == 1                # floor
 
 
-def test_reopt_normal_equations(orc):
+def test_reopt_normal_equations(orc_any):
     """support = all p, huge M, tiny lambda2 -> least squares."""
-    O = orc
+    O = orc_any
     rng = np.random.default_rng(5)
     X = rng.normal(size=(40, 3))
     y = X @ np.array([1.0, -2.0, 0.5]) + 0.01 * rng.normal(size=40)
@@ -158,9 +158,9 @@ def test_reopt_normal_equations(orc):
     assert abs(objs[1] - 0.5 * np.sum(y ** 2)) < 1e-9
 
 
-def test_solve_zero_response(orc):
+def test_solve_zero_response(orc_any):
     """y = 0 -> value 0."""
-    O = orc
+    O = orc_any
     rng = np.random.default_rng(6)
     inst = O.Instance(np.asfortranarray(rng.normal(size=(20, 6))), np.zeros(20), O.SQUARED, 2,
                       2.0, 1.0)
