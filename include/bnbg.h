@@ -136,6 +136,14 @@ int bnbg_relax_batch(bnbg_handle* h, const bnbg_relax_cfg* cfg, int m, const uin
                      double* beta_out, double* bounds_out, int32_t* status_out,
                      int32_t* iters_out, bnbg_trace_fn trace, void* user);
 
+/* prox_kernel.hpp:52-90 BatchMeta::from_nodes -- the device packer (VK1)
+ * alone.  J0 / J1 lists as CSR (j0_off[m+1], j0_idx; j1_off[m+1], j1_idx;
+ * 0-based, disjoint per node) -> state_out p x m CoordState bytes (column b
+ * = node b), kbar_out[m] = max(0, k - |J1|), free_count_out[m] = |Jf|. */
+int bnbg_pack_batch(bnbg_handle* h, int m, const int32_t* j0_off, const int32_t* j0_idx,
+                    const int32_t* j1_off, const int32_t* j1_idx, uint8_t* state_out,
+                    int32_t* kbar_out, int32_t* free_count_out);
+
 /* primal_heuristics.hpp:134-146 round_support, batched.  fixed_one lists in
  * construction order as CSR (one_off[m+1], one_idx).  support_out is m x k
  * (row b holds J1 ++ top-kbar free), len_out[m]. */

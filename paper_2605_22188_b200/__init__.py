@@ -436,6 +436,30 @@ class Engine:
         return RelaxationResult(beta.T.copy(), bounds, status, iters)
 
     # -- primal_heuristics.hpp:134-163 ----------------------------------------
+    # -- prox_kernel.hpp:52-90 BatchMeta::from_nodes (the device packer) -------
+    def pack_batch(self, nodes: Sequence[NodeState]):
+        """Returns (state p x m uint8 CoordState, reduced_budget[m], free_count[m])
+        as built on the device by the packer (VK1)."""
+        m, p = len(nodes), self.inst.p()
+        if m == 0:
+            raise InputError("batch meta: empty batch")
+
+        def csr(lists):
+            off = np.zeros(m + 1, dtype=np.int32)
+            for b, lst in enumerate(lists):
+                off[b + 1] = off[b] + len(lst)
+            idx = np.ascontiguousarray([j for lst in lists for j in lst] or [0], dtype=np.int32)
+            return off, idx
+
+        z_off, z_idx = csr([nd.fixed_zero for nd in nodes])
+        o_off, o_idx = csr([nd.fixed_one for nd in nodes])
+        state = np.zeros(p * m, dtype=np.uint8)
+        kbar = np.zeros(m, dtype=np.int32)
+        free = np.zeros(m, dtype=np.int32)
+        _check(_L.lib().bnbg_pack_batch(self._h, m, z_off, z_idx, o_off, o_idx, state, kbar, free),
+               self._h)
+        return state.reshape(m, p).T.copy(), kbar.tolist(), free.tolist()
+
     def round_support_batch(self, beta: np.ndarray, nodes: Sequence[NodeState]) -> List[List[int]]:
         p, m = beta.shape
         k = self.inst.k

@@ -65,7 +65,8 @@ up = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
 EXPORTS = [
     "bnbg_relax_cfg_default", "bnbg_solver_cfg_default", "bnbg_auto_batch_size",
     "bnbg_generate_synthetic", "bnbg_validate", "bnbg_create", "bnbg_destroy",
-    "bnbg_last_error", "bnbg_smoothness", "bnbg_relax_batch", "bnbg_round_support",
+    "bnbg_last_error", "bnbg_smoothness", "bnbg_relax_batch", "bnbg_pack_batch",
+    "bnbg_round_support",
     "bnbg_select_branch", "bnbg_reoptimize", "bnbg_prox_step", "bnbg_conjugate_prox",
     "bnbg_g_value", "bnbg_g_conjugate", "bnbg_gemm", "bnbg_solve", "bnbg_collect_rashomon",
     "bnbg_pool_size", "bnbg_pool_record", "bnbg_pool_free", "bnbg_kernel_launches",
@@ -103,6 +104,7 @@ def lib():
                                    TRACE_FN, vp]
     L.bnbg_round_support.argtypes = [vp, i, dp, up, ip, ip, ip, ip, ip]
     L.bnbg_select_branch.argtypes = [vp, i, dp, up, ip]
+    L.bnbg_pack_batch.argtypes = [vp, i, ip, ip, ip, ip, up, ip, ip]
     L.bnbg_reoptimize.argtypes = [vp, i, ip, ip, dp, dp]
     L.bnbg_prox_step.argtypes = [i, i, i, dp, d, d, up, ip, d, dp]
     L.bnbg_conjugate_prox.argtypes = [i, i, i, dp, d, up, ip, d, dp]

@@ -735,6 +735,39 @@ int bnbg_relax_batch(bnbg_handle* h, const bnbg_relax_cfg* cfg, int m, const uin
   return BNBG_OK;
 }
 
+int bnbg_pack_batch(bnbg_handle* h, int m, const int32_t* j0_off, const int32_t* j0_idx,
+                    const int32_t* j1_off, const int32_t* j1_idx, uint8_t* state_out,
+                    int32_t* kbar_out, int32_t* free_count_out) {
+  end_pool_pass(h);
+  if (m <= 0) return set_err(h, BNBG_INPUT_ERROR, "batch meta: empty batch");
+  const int p = h->eng.p;
+  bnbg::BatchLists L;
+  L.m = m;
+  std::vector<uint8_t> mark(p);
+  for (int b = 0; b < m; ++b) {
+    std::fill(mark.begin(), mark.end(), 0);
+    for (int pass = 0; pass < 2; ++pass) {
+      const int32_t* off = pass ? j1_off : j0_off;
+      const int32_t* idx = pass ? j1_idx : j0_idx;
+      if (off[b + 1] < off[b]) return set_err(h, BNBG_INPUT_ERROR, "batch meta: bad offsets");
+      for (int t = off[b]; t < off[b + 1]; ++t) {
+        if (idx[t] < 0 || idx[t] >= p)
+          return set_err(h, BNBG_INPUT_ERROR, "batch meta: index out of range");
+        if (mark[idx[t]]++)
+          return set_err(h, BNBG_INPUT_ERROR, "batch meta: J0 and J1 must be disjoint sets");
+      }
+    }
+  }
+  L.z_off.assign(j0_off, j0_off + m + 1);
+  L.o_off.assign(j1_off, j1_off + m + 1);
+  L.z_idx.assign(j0_idx + j0_off[0], j0_idx + j0_off[m]);
+  L.o_idx.assign(j1_idx + j1_off[0], j1_idx + j1_off[m]);
+  for (auto& v : L.z_off) v -= j0_off[0];
+  for (auto& v : L.o_off) v -= j1_off[0];
+  const int rc = h->eng.pack_lists(L, state_out, kbar_out, free_count_out);
+  return rc ? set_err(h, rc, h->eng.err) : BNBG_OK;
+}
+
 int bnbg_round_support(bnbg_handle* h, int m, const double* beta, const uint8_t* state,
                        const int32_t* kbar, const int32_t* one_off, const int32_t* one_idx,
                        int32_t* support_out, int32_t* len_out) {

@@ -825,6 +825,37 @@ int Engine::relax_lists(const BatchLists& L_, const double* warm, const RelaxPar
   return relax_uploaded(m, cfg, thr, trace, out, true, do_off, do_idx, nullptr, true);
 }
 
+int Engine::pack_lists(const BatchLists& L_, uint8_t* state_out, int* kbar_out, int* pf_out) {
+  const int m = L_.m;
+  if (m <= 0) return fail(1, "batch meta: empty batch");
+  if (int rc = ensure(m)) return rc;
+  const size_t nz = L_.z_idx.size(), no = L_.o_idx.size();
+  const size_t ints = (size_t)(m + 1) * 2 + nz + no;
+  const size_t bytes = sizeof(double) * (size_t)p * m + sizeof(int) * (ints + 4);
+  if (int rc = ensure_aux(bytes)) return rc;
+  double* dWarm = static_cast<double*>(dAux_);
+  int* dz_off = reinterpret_cast<int*>(dWarm + (size_t)p * m);
+  int* do_off = dz_off + (m + 1);
+  int* dz_idx = do_off + (m + 1);
+  int* do_idx = dz_idx + nz;
+  CK(cudaMemsetAsync(dWarm, 0, sizeof(double) * (size_t)p * m, stream_));
+  if (int rc_ = h2d(dz_off, L_.z_off.data(), sizeof(int) * (m + 1))) return rc_;
+  if (int rc_ = h2d(do_off, L_.o_off.data(), sizeof(int) * (m + 1))) return rc_;
+  if (nz)
+    if (int rc_ = h2d(dz_idx, L_.z_idx.data(), sizeof(int) * nz)) return rc_;
+  if (no)
+    if (int rc_ = h2d(do_idx, L_.o_idx.data(), sizeof(int) * no)) return rc_;
+  k_pack<<<m, 256, 0, stream_>>>(p, k, m, dz_off, dz_idx, do_off, do_idx, dState_, dKbar_, dPf_,
+                                 dWarm, dB_, dV_, dT_, dBest_, dLast_, dFrozen_, dStatus_, dIters_,
+                                 dAct_, 1);
+  CKL("k_pack");
+  if (int rc_ = d2h(state_out, dState_, (size_t)p * m)) return rc_;
+  if (int rc_ = d2h(kbar_out, dKbar_, sizeof(int) * m)) return rc_;
+  if (int rc_ = d2h(pf_out, dPf_, sizeof(int) * m)) return rc_;
+  CK(cudaStreamSynchronize(stream_));
+  return 0;
+}
+
 int Engine::round_select(int m, const double* beta, const uint8_t* state, const int32_t* kbar,
                          const int32_t* one_off, const int32_t* one_idx, int32_t* sup,
                          int32_t* len, int32_t* jb) {

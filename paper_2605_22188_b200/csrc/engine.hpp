@@ -65,6 +65,8 @@ class Engine {
   // one BnB pass of lower bounds + rounding + branch selection from CSR lists
   int relax_lists(const BatchLists& lists, const double* warm, const RelaxParams& cfg,
                   double prune_threshold, bool trace, PassResult& out);
+  // the packer alone (bnbg_pack_batch): CSR lists -> state, kbar, free count
+  int pack_lists(const BatchLists& lists, uint8_t* state_out, int* kbar_out, int* pf_out);
   // reoptimize_supports (CSR)
   int reoptimize(int nsup, const int* offsets, const int* idx, double* coef, double* obj);
   int round_select(int m, const double* beta, const uint8_t* state, const int32_t* kbar,

@@ -505,6 +505,7 @@ static __global__ void k_pack(int p, int k, int m, const int* z_off, const int* 
   __syncthreads();
   const int z0 = z_off[b], z1 = z_off[b + 1], q0 = o_off[b], q1 = o_off[b + 1];
   for (int t2 = z0 + threadIdx.x; t2 < z1; t2 += blockDim.x) col[z_idx[t2]] = kFixedZero;
+  __syncthreads();  // J1 after J0, as prox_kernel.hpp:73-80
   for (int t2 = q0 + threadIdx.x; t2 < q1; t2 += blockDim.x) col[o_idx[t2]] = kFixedOne;
   if (threadIdx.x == 0) {
     const int kb = k - (q1 - q0);
