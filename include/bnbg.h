@@ -280,6 +280,11 @@ int bnbg_kernel_stats(const bnbg_handle* h, int kernel_class, double* ms, double
 int bnbg_pass_profile(const bnbg_handle* h, double* ns_out, int count);
 /* Host<->device bytes copied by this handle so far. */
 int bnbg_transfer_bytes(const bnbg_handle* h, long long* h2d, long long* d2h);
+/* Last bnbg_solve_sharded on this handle: out[0] node records sent, out[1]
+ * received through the load-balance exchange, out[2] passes, then the local
+ * relaxation batch width of each pass.  Returns the number of values (may
+ * exceed cap; only cap are written). */
+int bnbg_shard_stats(const bnbg_handle* h, long long* out, int cap);
 
 #ifdef __cplusplus
 }

@@ -392,6 +392,14 @@ class Engine:
         _L.lib().bnbg_pass_profile(self._h, buf, len(buf))
         return buf
 
+    def shard_stats(self):
+        """Last sharded solve on this engine: {"sent", "received", "batch_per_pass"}."""
+        cap = 1 << 16
+        buf = (C.c_longlong * cap)()
+        cnt = _L.lib().bnbg_shard_stats(self._h, buf, cap)
+        vals = list(buf[:min(cnt, cap)])
+        return {"sent": vals[0], "received": vals[1], "batch_per_pass": vals[3:]}
+
     def transfer_bytes(self):
         a, b = C.c_longlong(), C.c_longlong()
         _L.lib().bnbg_transfer_bytes(self._h, C.byref(a), C.byref(b))

@@ -73,6 +73,7 @@ EXPORTS = [
     "bnbg_gemm_stats", "bnbg_set_timing", "bnbg_kernel_stats", "bnbg_transfer_bytes",
     "bnbg_pass_profile", "bnbg_nccl_unique_id", "bnbg_nccl_init", "bnbg_solve_sharded",
     "bnbg_balance_plan", "bnbg_pool_root", "bnbg_pool_relax", "bnbg_pool_branch",
+    "bnbg_shard_stats",
 ]
 
 
@@ -105,6 +106,7 @@ def lib():
     L.bnbg_round_support.argtypes = [vp, i, dp, up, ip, ip, ip, ip, ip]
     L.bnbg_select_branch.argtypes = [vp, i, dp, up, ip]
     L.bnbg_pack_batch.argtypes = [vp, i, ip, ip, ip, ip, up, ip, ip]
+    L.bnbg_shard_stats.argtypes = [vp, C.POINTER(C.c_longlong), i]
     L.bnbg_reoptimize.argtypes = [vp, i, ip, ip, dp, dp]
     L.bnbg_prox_step.argtypes = [i, i, i, dp, d, d, up, ip, d, dp]
     L.bnbg_conjugate_prox.argtypes = [i, i, i, dp, d, up, ip, d, dp]

@@ -8,6 +8,8 @@
 // as one device batch.  Only the queue bookkeeping and child construction
 // (node_model.hpp:77-105) stay on the host.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -28,6 +30,10 @@ struct bnbg_handle {
   bnbg::Engine eng;
   int last_pool_m = 0;                 // batch of the last bnbg_pool_relax
   std::vector<int> last_pool_slots;
+  // last sharded solve on this rank: node records sent / received through
+  // the pool exchange, and the relaxation batch width of every pass
+  long long shard_sent = 0, shard_recv = 0;
+  std::vector<int> shard_batch;
 };
 
 struct bnbg_pool {
@@ -188,6 +194,38 @@ bnbg::RelaxParams relax_params(const bnbg_relax_cfg& c) {
   return r;
 }
 
+// reoptimize_supports (primal_heuristics.hpp:174-227) is a pure function of
+// each support SEQUENCE (indices in order: the order fixes the summation
+// order of X_S beta), so equal sequences give bit-identical coefficients and
+// objectives.  Deep passes round many nodes to the same sequence; each
+// distinct one is re-optimised once and the results are scattered back.
+static int reoptimize_unique(bnbg::Engine& eng, int nsup, const std::vector<int>& off,
+                             const std::vector<int>& idx, double* coef, double* obj) {
+  std::map<std::vector<int>, int> seen;
+  std::vector<int> first(nsup), uoff(1, 0), uidx;
+  for (int s = 0; s < nsup; ++s) {
+    std::vector<int> key(idx.begin() + off[s], idx.begin() + off[s + 1]);
+    auto it = seen.find(key);
+    if (it == seen.end()) {
+      const int u = (int)uoff.size() - 1;
+      it = seen.emplace(std::move(key), u).first;
+      uidx.insert(uidx.end(), idx.begin() + off[s], idx.begin() + off[s + 1]);
+      uoff.push_back((int)uidx.size());
+    }
+    first[s] = it->second;
+  }
+  const int nu = (int)uoff.size() - 1;
+  if (nu == nsup) return eng.reoptimize(nsup, off.data(), idx.data(), coef, obj);
+  std::vector<double> ucoef(uidx.size() + 1), uobj(nu + 1);
+  if (int rc = eng.reoptimize(nu, uoff.data(), uidx.data(), ucoef.data(), uobj.data())) return rc;
+  for (int s = 0; s < nsup; ++s) {
+    const int u = first[s];
+    std::copy(ucoef.begin() + uoff[u], ucoef.begin() + uoff[u + 1], coef + off[s]);
+    obj[s] = uobj[u];
+  }
+  return 0;
+}
+
 // Incumbent record exchanged between ranks: objective, |support|, support
 // (sorted) and coefficients, as doubles.
 struct IncRecord {
@@ -259,6 +297,15 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
     }
     return 0;
   };
+  // Test instrumentation (BNBG_FAULT="rank:pass"): that rank's pass fails
+  // with a numeric error, exercising the error path of the collectives.
+  int fault_rank = -1, fault_pass = -1;
+  if (comm) {
+    h->shard_sent = h->shard_recv = 0;
+    h->shard_batch.clear();
+    if (const char* f = getenv("BNBG_FAULT")) sscanf(f, "%d:%d", &fault_rank, &fault_pass);
+  }
+  int pass_no = 0;
   // After a collective: the lowest-ranked failure ends the solve on all ranks.
   auto collective_error = [&](const double* codes, size_t stride) -> int {
     for (int r = 0; r < world; ++r) {
@@ -304,6 +351,12 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
     }
     const int m = (int)batch_slots.size();
     if (!comm && m == 0 && leaves.empty()) continue;
+    if (comm) {
+      h->shard_batch.push_back(m);
+      if (rank == fault_rank && pass_no == fault_pass)
+        if (int e = fail(BNBG_NUMERIC_ERROR, "injected fault (BNBG_FAULT)")) return e;
+    }
+    ++pass_no;
 
     if (m > 0) {
       Timer t(cert->lower_bound_seconds);
@@ -347,7 +400,7 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
     std::vector<double> coef(sidx.size() + 1), obj(nsup + 1);
     if (nsup > 0 && !pass_rc) {
       Timer t(cert->reoptimization_seconds);
-      const int rc = eng.reoptimize(nsup, offsets.data(), sidx.data(), coef.data(), obj.data());
+      const int rc = reoptimize_unique(eng, nsup, offsets, sidx, coef.data(), obj.data());
       if (rc) {
         if (int e = fail(rc, eng.err)) return e;
       }
@@ -491,6 +544,8 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
         if (int rc = comm->exchange(eng, send_n, d_send, recv_n, d_recv, eng.node_record_bytes()))
           return set_err(h, rc, eng.err);
         for (int s : send_slots) slots.give(s);
+        h->shard_sent += nsend;
+        h->shard_recv += nrecv;
         if (nrecv > 0) {
           std::vector<int> rslots(nrecv);
           for (auto& s : rslots) s = slots.take();
@@ -1007,6 +1062,15 @@ int bnbg_kernel_stats(const bnbg_handle* h, int kc, double* ms, double* flops,
 
 int bnbg_pass_profile(const bnbg_handle* h, double* ns_out, int count) {
   return const_cast<bnbg_handle*>(h)->eng.pass_profile(ns_out, count);
+}
+
+int bnbg_shard_stats(const bnbg_handle* h, long long* out, int cap) {
+  const int np = (int)h->shard_batch.size();
+  if (cap >= 1) out[0] = h->shard_sent;
+  if (cap >= 2) out[1] = h->shard_recv;
+  if (cap >= 3) out[2] = np;
+  for (int i = 0; i < np && 3 + i < cap; ++i) out[3 + i] = h->shard_batch[i];
+  return 3 + np;
 }
 
 int bnbg_transfer_bytes(const bnbg_handle* h, long long* h2d, long long* d2h) {

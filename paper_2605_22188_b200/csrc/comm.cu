@@ -3,6 +3,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -240,8 +242,19 @@ bool balance_plan(int world, const int64_t* counts, int64_t* moves) {
     mx = std::max(mx, counts[r]);
     mn = std::min(mn, counts[r]);
   }
+  // skew rule max > factor * min + slack; BNBG_BALANCE_SKEW="factor,slack"
+  // (default "2,8"; "1,0" rebalances whenever the queues differ -- tests use
+  // it to push many node records through the exchange)
+  int64_t factor = 2, slack = 8;
+  if (const char* e = getenv("BNBG_BALANCE_SKEW")) {
+    long long f = 2, s = 8;
+    if (sscanf(e, "%lld,%lld", &f, &s) == 2 && f >= 1 && s >= 0) {
+      factor = f;
+      slack = s;
+    }
+  }
   const bool starving = mn == 0 && mx >= 2;
-  const bool skewed = mx > 2 * mn + 8;
+  const bool skewed = mx > factor * mn + slack;
   if (world < 2 || !(starving || skewed)) return false;
   std::vector<int64_t> surplus(world), deficit(world);
   for (int r = 0; r < world; ++r) {

@@ -8,6 +8,9 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
+
 #include "engine.hpp"
 #include "gemm.cuh"
 #include "node_kernels.cuh"
@@ -90,6 +93,14 @@ Engine::~Engine() {
   dfree(dPassOut_);
   dfree(dPassProf_);
   dfree(dBar_);
+  dfree(dTmap_);
+  for (OzSide& S : oz_) {
+    dfree(S.dX);
+    dfree(S.dEx);
+    dfree(S.dB);
+    dfree(S.dEb);
+    dfree(S.dTm);
+  }
   comm_release();
   for (void* q : pool_mem_) dfree(q);
   dfree(dSlots_);
@@ -110,6 +121,49 @@ Engine::~Engine() {
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
   if (stream_) cudaStreamDestroy(stream_);
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// X (n x p column-major, resident) as a 2-D FLOAT64 tensor {n, p}: one map
+// per A-tile box of the register-tiled GEMM (BNBG_TMA=0 keeps cp.async).
+int Engine::make_tmaps() {
+  const char* e = getenv("BNBG_TMA");
+  if ((e && e[0] == '0') || (n % 2) || (p % 2)) return 0;
+  auto enc = tmap_encoder();
+  if (!enc) return fail(4, "cuTensorMapEncodeTiled unavailable");
+  int nn[2], tn[2];
+  gemm_big_boxes(nn, tn);
+  CUtensorMap h[2];
+  const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)p};
+  const cuuint64_t strides[1] = {(cuuint64_t)n * sizeof(double)};
+  const cuuint32_t estr[2] = {1, 1};
+  for (int t = 0; t < 2; ++t) {
+    const cuuint32_t box[2] = {(cuuint32_t)(t ? tn[0] : nn[0]), (cuuint32_t)(t ? tn[1] : nn[1])};
+    const CUresult r = enc(&h[t], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, dX_, dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return fail(4, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  }
+  CK(cudaMallocAsync(&dTmap_, sizeof(h), stream_));
+  CK(cudaMemcpyAsync(dTmap_, h, sizeof(h), cudaMemcpyHostToDevice, stream_));
+  CK(cudaStreamSynchronize(stream_));
+  tmNN_ = dTmap_;
+  tmTN_ = static_cast<const char*>(dTmap_) + sizeof(CUtensorMap);
+  return 0;
 }
 
 int Engine::fail(int code, const std::string& msg) {
@@ -163,6 +217,7 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
   if (int rc_ = h2d(dX_, X, sizeof(double) * (size_t)n * p)) return rc_;
   if (int rc_ = h2d(dy_, y, sizeof(double) * (size_t)n)) return rc_;
   stamp("upload");
+  if (int rc = make_tmaps()) return rc;
   CK(cudaMallocAsync(&dMa_, sizeof(int), stream_));
   CK(cudaMallocAsync(&dErr_, sizeof(int), stream_));
   CK(gemm_set_attrs());
@@ -362,12 +417,22 @@ Engine::GemmPlan Engine::plan(int Mr, int K, int ncols, bool allow_split) const 
   GemmPlan pl;
   // wide batches: register-tiled 128 x 64 tiles, no split-K (BNBG_BIGGEMM=0 disables)
   if (big_min_ > 0 && ncols >= big_min_ && (n % 2) == 0 && (p % 2) == 0) {
-    const int bm = gemm_big_tile_m(), bn = gemm_big_tile_n();
+    const int bm = gemm_big_tile_m(), bn = gemm_big_tile_n(), bk = gemm_big_tile_k();
     pl.big = true;
     pl.fm = pl.fn = 0;
-    pl.nsplit = 1;
-    pl.ksplit = K;
-    pl.grid = dim3((Mr + bm - 1) / bm, (ncols + bn - 1) / bn, 1);
+    const int mt = (Mr + bm - 1) / bm, nt = (ncols + bn - 1) / bn;
+    // TN: split K until the tiles fill both CTA slots of every SM (c4 at
+    // m_a <= 64: 40 tiles on 148 SMs unsplit), keeping >= 32 k-tiles a split
+    int nsplit = 1;
+    if (allow_split) {
+      const int nkt = (K + bk - 1) / bk;
+      while (nsplit < nsplit_max_ && mt * nt * nsplit < 2 * sms_ && nkt >= 2 * nsplit * 32)
+        nsplit *= 2;
+    }
+    const int nkt = (K + bk - 1) / bk;
+    pl.ksplit = ((nkt + nsplit - 1) / nsplit) * bk;
+    pl.nsplit = (K + pl.ksplit - 1) / pl.ksplit;
+    pl.grid = dim3(mt, nt, pl.nsplit);
     return pl;
   }
   pl.fn = ncols <= 8 ? 1 : (ncols <= 16 ? 2 : 4);
@@ -418,6 +483,7 @@ int Engine::launch_gemm(bool tn, int epi, const GemmPlan& pl, const double* Bsrc
   g.part_conj = dPC_;
   g.part_ld = part_ld;
   ++launches;
+  g.tmap = pl.big ? (tn ? tmTN_ : tmNN_) : nullptr;
   if (pl.big)
     CK(gemm_big_launch(tn, epi, pl.grid, stream_, g));
   else
@@ -496,15 +562,24 @@ int Engine::compute_smoothness(double* out) {
 int Engine::step(int ma, double eta, double rho, const RelaxParams& cfg) {
   const GemmPlan p1 = plan(n, p, ma, false);
   tic(KC_GEMM_NN);
-  if (int rc = launch_gemm(false, EPI_DERIV, p1, dV_, p, dR_, n, dAct_, dMa_, 0, mcap_)) return rc;
+  if (p1.big && ozaki_enabled()) {  // tcgen05 kind::i8 emulated FP64 + l' epilogue
+    if (int rc = gemm_ozaki(false, true, dV_, p, dAct_, ma, dMa_, dR_, n, 0, nullptr)) return rc;
+  } else if (int rc = launch_gemm(false, EPI_DERIV, p1, dV_, p, dR_, n, dAct_, dMa_, 0, mcap_)) {
+    return rc;
+  }
   toc(KC_GEMM_NN, 2.0 * n * p * ma);
   const GemmPlan p2 = plan(p, n, ma, true);
   tic(KC_GEMM_TN);
-  if (int rc = launch_gemm(true, EPI_STORE, p2, dR_, n, dG_, p, dAct_, dMa_,
-                           (long long)p * mcap_, mcap_))
+  int tn_split = p2.nsplit;
+  if (p2.big && ozaki_enabled()) {  // tcgen05 kind::i8 emulated FP64 (ozaki.cuh)
+    if (int rc = gemm_ozaki(true, false, dR_, n, dAct_, ma, dMa_, dG_, p, (long long)p * mcap_, &tn_split))
+      return rc;
+  } else if (int rc = launch_gemm(true, EPI_STORE, p2, dR_, n, dG_, p, dAct_, dMa_,
+                                  (long long)p * mcap_, mcap_)) {
     return rc;
+  }
   toc(KC_GEMM_TN, 2.0 * n * p * ma);
-  cur_nsplit_ = p2.nsplit;
+  cur_nsplit_ = tn_split;
   RelaxDev r{};
   r.p = p;
   r.n2 = n2_;
@@ -513,7 +588,7 @@ int Engine::step(int ma, double eta, double rho, const RelaxParams& cfg) {
   r.V = dV_;
   r.G = dG_;
   r.split_stride = (long long)p * mcap_;
-  r.nsplit = p2.nsplit;
+  r.nsplit = tn_split;
   r.state = dState_;
   r.kbar = dKbar_;
   r.pf = dPf_;
@@ -677,6 +752,8 @@ int Engine::run_pass(int m, const RelaxParams& cfg, double thr, double eta, doub
   a.bar = dBar_;
   a.res = res_;
   a.big = ((n % 2) == 0 && (p % 2) == 0) ? big_min_ : 0;
+  a.nn.tmap = res_.on ? nullptr : tmNN_;  // streaming mode's 128 x 64 tiles
+  a.tn.tmap = res_.on ? nullptr : tmTN_;
   CK(cudaMemsetAsync(dBar_, 0, sizeof(unsigned), stream_));
   tic(KC_PASS);
   cudaError_t e = cudaSuccess;
@@ -1030,15 +1107,21 @@ int Engine::gemm_probe(int trans, int m, const double* Bh, double* Ch) {
   if (int rc_ = h2d(dBin, Bh, sizeof(double) * (size_t)K * m)) return rc_;
   if (int rc_ = h2d(dMa_, &m, sizeof(int))) return rc_;
   const GemmPlan pl = plan(Mo, K, m, trans != 0);
-  if (int rc = launch_gemm(trans != 0, EPI_STORE, pl, dBin, K, dC, Mo, nullptr, dMa_,
-                           (long long)Mo * m, m))
+  int ns = pl.nsplit;
+  if (pl.big && ozaki_enabled()) {
+    if (int rc = gemm_ozaki(trans != 0, false, dBin, K, nullptr, m, dMa_, dC, Mo,
+                            (long long)Mo * m, &ns))
+      return rc;
+  } else if (int rc = launch_gemm(trans != 0, EPI_STORE, pl, dBin, K, dC, Mo, nullptr, dMa_,
+                                  (long long)Mo * m, m)) {
     return rc;
-  std::vector<double> slabs((size_t)Mo * m * pl.nsplit);
+  }
+  std::vector<double> slabs((size_t)Mo * m * ns);
   if (int rc_ = d2h(slabs.data(), dC, sizeof(double) * slabs.size())) return rc_;
   CK(cudaStreamSynchronize(stream_));
   for (size_t e = 0; e < (size_t)Mo * m; ++e) {
     double s = slabs[e];
-    for (int t = 1; t < pl.nsplit; ++t) s += slabs[(size_t)t * Mo * m + e];
+    for (int t = 1; t < ns; ++t) s += slabs[(size_t)t * Mo * m + e];
     Ch[e] = s;
   }
   return 0;

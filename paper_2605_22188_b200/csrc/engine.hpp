@@ -162,6 +162,26 @@ class Engine {
   size_t pass_smem_ = 0;
   long long* dPassOut_ = nullptr;
   unsigned* dBar_ = nullptr;  // grid barrier counter of the pass kernel
+  // TMA descriptors of X (global memory) for the 128 x 64 tiles' A operand:
+  // NN box and TN box (gemm_big.cuh); nullptr when TMA staging is off
+  void* dTmap_ = nullptr;
+  const void* tmNN_ = nullptr;
+  const void* tmTN_ = nullptr;
+  int make_tmaps();
+  // tcgen05 kind::i8 emulated-FP64 TN product (ozaki.cu; BNBG_OZAKI=1)
+  bool ozaki_enabled() const;
+  int ozaki_prepare_x(int side);
+  int ozaki_reserve_b(int side, int m);
+  int gemm_ozaki(bool tn, bool deriv, const double* Bsrc, int ldb, const int* act, int ma,
+                 const int* d_ncols, double* C, int ldc, long long split_stride, int* nsplit);
+  struct OzSide {             // [0] NN (X rows), [1] TN (X columns)
+    void* dX = nullptr;       // X digits [kOzS][rows][kpad] int8
+    int* dEx = nullptr;       // per-row exponent
+    void* dB = nullptr;       // batch digits [kOzS][bcap][kpad]
+    int* dEb = nullptr;
+    void* dTm = nullptr;      // CUtensorMaps: X digits, batch digits
+    int kpad = 0, bcap = 0;
+  } oz_[2];
   ResLayout res_{};           // X residency plan (res_.on = 0: streaming)
  public:
   unsigned long long* dPassProf_ = nullptr;  // phase wall times (BNBG_PASS_PROF=1)

@@ -42,6 +42,9 @@ struct GemmArgs {
   double* part_conj;
   int part_ld;
   unsigned long long* probe;  // optional sub-phase timers (CTA 0), nullptr: off
+  // TMA descriptor (CUtensorMap in global memory) of X for the 128 x 64
+  // register-tiled kernel's A tiles (gemm_big.cuh); nullptr: cp.async staging
+  const void* tmap;
 };
 
 constexpr int kGemmThreads = 128;
@@ -214,7 +217,7 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int ncols, int mt, 
 
 template <bool TN, int FM, int FN, int EPI>
 __global__ void __launch_bounds__(kGemmThreads) k_gemm(GemmArgs g) {
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double smem[];
   __shared__ int colmap[32];
   const int ncols = *g.d_ncols;
   if ((int)blockIdx.y * GemmShape<TN, FM, FN>::BN >= ncols) return;

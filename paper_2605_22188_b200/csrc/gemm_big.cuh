@@ -5,11 +5,19 @@
 // kernel's cross-warp reductions cost more than they hide:
 //   CTA tile 128 x 64, 8 warps in a 4 (M) x 2 (N) grid, warp tile 32 x 32
 //   (4 x 4 DMMA.8x8x4 fragments, 16 independent accumulators per lane),
-//   BK = 16 (four k-steps) staged through a 3-deep 16-byte cp.async ring
-//   (90 KB: two CTAs, 16 warps per SM).
+//   BK = 16 (four k-steps) staged through a 3-deep ring (90 KB: two CTAs,
+//   16 warps per SM).
+// Staging: the X tile of a stage (the A operand, 2/3 of the bytes) is one
+// TMA box (cp.async.bulk.tensor.2d, UTMALDG) completing on the stage's
+// mbarrier; the box is 4 elements wider than the tile so the shared-memory
+// rows land on the conflict-free (= 4 mod 16 doubles) stride the fragment
+// loads need, and TMA zero-fills past n and p.  The B operand (columns
+// gathered through the active list) is cp.async 16-byte chunks.
+// TN (G = X' R) splits K over blockIdx.z when the tiles alone leave SMs
+// idle (c4: p / 128 = 40 row tiles); slab s holds rows [s*ksplit, ...) and
+// the consumers sum the slabs in order.
 // Every output element is accumulated by one lane in k order, so results are
-// deterministic.  Shared-memory strides are = 4 (mod 16) doubles, which makes
-// the fragment loads conflict-free.  Needs n and p even (16-byte rows).
+// deterministic.  Needs n and p even (16-byte rows).
 #pragma once
 #include "gemm.cuh"
 
@@ -30,13 +38,66 @@ constexpr int kBigB = kBigBN * kBigLDK;
 constexpr int kBigStage = kBigA + kBigB;
 constexpr size_t kBigSmemBytes = sizeof(double) * (size_t)kBigNS * kBigStage;
 
+// TMA boxes (elements, innermost first) of X = n x p column-major:
+//   NN  A(m, k) = X[k*n + m0 + m], stored [k][kBigLDA_NN]: box {kBigLDA_NN, kBigBK}
+//   TN  A(m, k) = X[(m0+m)*n + k0 + k], stored [m][kBigLDK]: box {kBigLDK, kBigBM}
+constexpr int kBigBoxNN0 = kBigLDA_NN, kBigBoxNN1 = kBigBK;
+constexpr int kBigBoxTN0 = kBigLDK, kBigBoxTN1 = kBigBM;
+constexpr unsigned kBigTxNN = sizeof(double) * kBigBoxNN0 * kBigBoxNN1;
+constexpr unsigned kBigTxTN = sizeof(double) * kBigBoxTN0 * kBigBoxTN1;
+static_assert(kBigBoxNN0 * kBigBoxNN1 <= kBigA && kBigBoxTN0 * kBigBoxTN1 <= kBigA, "box fits");
+static_assert((kBigStage * sizeof(double)) % 128 == 0, "TMA destinations 128-byte aligned");
+
+// one mbarrier per ring stage and the parity of each (bit s), per CTA
+static __shared__ __align__(8) unsigned long long s_big_bar[kBigNS];
+static __shared__ unsigned s_big_phase;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// Once per CTA before the first gemm_big_tile of a kernel (all threads call).
+__device__ __forceinline__ void gemm_big_tma_init() {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kBigNS; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_big_bar[s])));
+    s_big_phase = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int c0, int c1,
+                                            unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // One 128 x BN output tile (row tile mt, column tile nt), BN = 64 (warp tile
 // 32 x 32) or 32 (warp tile 32 x 16, for narrower batches).  All 256 threads
 // of the CTA call; smem holds kBigSmemBytes; colmap kBigBN ints and epi_red
 // 2 x 4 x kBigBN doubles of shared memory.  Ends with a block barrier.
 template <bool TN, int EPI, int BN = kBigBN>
 __device__ void gemm_big_tile(const GemmArgs& g, int ncols, int mt, int nt, double* smem,
-                              int* colmap, double (*epi_red)[4][kBigBN]) {
+                              int* colmap, double (*epi_red)[4][kBigBN], int split = 0) {
   static_assert(BN == 64 || BN == 32, "BN");
   constexpr int FN = BN / 16, WN = BN / 2;  // fragments and columns per warp
   const int n0 = nt * BN;
@@ -48,16 +109,31 @@ __device__ void gemm_big_tile(const GemmArgs& g, int ncols, int mt, int nt, doub
     colmap[tid] = c < ncols ? (g.act ? g.act[c] : c) : -1;
   }
   __syncthreads();
-  const int K = g.K;
-  const int nkt = (K + kBigBK - 1) / kBigBK;
+  // K range of this split (ksplit is a multiple of kBigBK: no stage straddles
+  // two splits, so the zero-fill at K covers the last one)
+  const int kbeg = TN ? split * g.ksplit : 0;
+  const int K = TN ? min(g.K, kbeg + g.ksplit) : g.K;
+  const int nkt = (K - kbeg + kBigBK - 1) / kBigBK;
+  const bool tma = g.tmap != nullptr;
+  unsigned phase = s_big_phase;
 
   auto load_stage = [&](int stage, int kt) {
     double* As = smem + stage * kBigStage;
     double* Bs = As + kBigA;
-    const int k0 = kt * kBigBK;
-    // A: 128 x BK doubles in 16-byte chunks
-    constexpr int KC = kBigBK / 2;  // chunks per k-row (TN) ...
+    const int k0 = kbeg + kt * kBigBK;
+    constexpr int KC = kBigBK / 2;  // 16-byte chunks per k-row (TN) ...
     constexpr int MC = kBigBM / 2;  // ... and per m-row (NN)
+    if (tma) {
+      if (threadIdx.x == 0) {
+        // the stage's previous contents were read by the generic proxy
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (TN)
+          tma_load_2d(As, g.tmap, k0, m0, &s_big_bar[stage], kBigTxTN);
+        else
+          tma_load_2d(As, g.tmap, m0, k0, &s_big_bar[stage], kBigTxNN);
+      }
+    } else {
+    // A: 128 x BK doubles in 16-byte chunks
 #pragma unroll
     for (int it = 0; it < kBigBM * kBigBK / 2 / kBigThreads; ++it) {
       const int e = tid + it * kBigThreads;
@@ -72,6 +148,7 @@ __device__ void gemm_big_tile(const GemmArgs& g, int ncols, int mt, int nt, doub
         const bool ok = gm < g.M && gk < K;
         cp_async_16(As + k * kBigLDA_NN + mc, ok ? g.A + (size_t)gk * g.lda + gm : g.A, ok ? 16 : 0);
       }
+    }
     }
     // B: BN columns x BK
 #pragma unroll
@@ -99,6 +176,11 @@ __device__ void gemm_big_tile(const GemmArgs& g, int ncols, int mt, int nt, doub
   }
   for (int kt = 0; kt < nkt; ++kt) {
     cp_async_wait<kBigNS - 2>();
+    if (tma) {
+      const int st = kt % kBigNS;
+      mbar_wait(&s_big_bar[st], (phase >> st) & 1u);
+      phase ^= 1u << st;
+    }
     __syncthreads();
     if (kt + kBigNS - 1 < nkt) load_stage((kt + kBigNS - 1) % kBigNS, kt + kBigNS - 1);
     cp_async_commit();
@@ -141,7 +223,7 @@ __device__ void gemm_big_tile(const GemmArgs& g, int ncols, int mt, int nt, doub
         if (gm >= g.M || col < 0) continue;
         const double s = acc[i][j][h];
         if (EPI == EPI_STORE) {
-          g.C[(size_t)col * g.ldc + gm] = s;
+          g.C[(size_t)split * g.split_stride + (size_t)col * g.ldc + gm] = s;
         } else {
           const double rv = d_loss_deriv(g.loss, s, yv);
           g.C[(size_t)col * g.ldc + gm] = rv;
@@ -186,17 +268,19 @@ __device__ void gemm_big_tile(const GemmArgs& g, int ncols, int mt, int nt, doub
       g.part_conj[(size_t)mt * g.part_ld + colmap[tid]] = sc;
     }
   }
+  if (tid == 0) s_big_phase = phase;
   __syncthreads();  // smem / colmap reusable by the caller's next tile
 }
 
 template <bool TN, int EPI>
-__global__ void __launch_bounds__(kBigThreads, 2) k_gemm_big(GemmArgs g) {
-  extern __shared__ __align__(16) double smem[];
+__global__ void __launch_bounds__(kBigThreads, 2) k_gemm_big(const __grid_constant__ GemmArgs g) {
+  extern __shared__ __align__(128) double smem[];
   __shared__ int colmap[kBigBN];
   __shared__ double epi_red[2][4][kBigBN];  // EVAL: per-warp-row column sums (l, l*)
   const int ncols = *g.d_ncols;
   if ((int)blockIdx.y * kBigBN >= ncols) return;
-  gemm_big_tile<TN, EPI>(g, ncols, blockIdx.x, blockIdx.y, smem, colmap, epi_red);
+  if (g.tmap) gemm_big_tma_init();
+  gemm_big_tile<TN, EPI>(g, ncols, blockIdx.x, blockIdx.y, smem, colmap, epi_red, blockIdx.z);
 }
 
 }  // namespace bnbg

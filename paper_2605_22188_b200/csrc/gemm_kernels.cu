@@ -36,6 +36,13 @@ cudaError_t gemm_set_attrs() {
 
 int gemm_big_tile_m() { return kBigBM; }
 int gemm_big_tile_n() { return kBigBN; }
+int gemm_big_tile_k() { return kBigBK; }
+void gemm_big_boxes(int* nn, int* tn) {
+  nn[0] = kBigBoxNN0;
+  nn[1] = kBigBoxNN1;
+  tn[0] = kBigBoxTN0;
+  tn[1] = kBigBoxTN1;
+}
 
 cudaError_t gemm_big_launch(bool tn, int epi, dim3 grid, cudaStream_t st, const GemmArgs& g) {
   const dim3 block(kBigThreads);

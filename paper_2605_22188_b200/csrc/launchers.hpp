@@ -52,6 +52,9 @@ cudaError_t gemm_launch(bool tn, int epi, int fm, int fn, dim3 grid, cudaStream_
 // register-tiled 128 x 64 DMMA GEMM for wide batches (gemm_big.cuh); n, p even
 int gemm_big_tile_m();
 int gemm_big_tile_n();
+int gemm_big_tile_k();
+// TMA box sizes {inner, outer} of the NN and TN A tiles (X)
+void gemm_big_boxes(int* nn, int* tn);
 cudaError_t gemm_big_launch(bool tn, int epi, dim3 grid, cudaStream_t st, const GemmArgs& g);
 
 // ---- column_kernels.cu -----------------------------------------------------

@@ -1,0 +1,153 @@
+// ozaki.cu -- Engine methods of the tcgen05 (kind::i8) emulated-FP64 products
+// of the relaxation iteration (ozaki.cuh):
+//   NN  R = l'(X V[:, act])   A = X  (rows i, k = j),  B = V  (k = j)
+//   TN  G = X' R[:, act]      A = X' (rows j, k = i),  B = R  (k = i)
+// X's digits are cut once per engine (both orientations, on first use);
+// the batch operand's digits every iteration.  The bound evaluation keeps
+// the DMMA kernels (Psi must be exact for the R it is evaluated at,
+// relaxation.hpp:125-147).  BNBG_OZAKI=1 enables the path.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
+#include "engine.hpp"
+#include "ozaki.cuh"
+
+namespace bnbg {
+
+#define CK(call)                                          \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);   \
+  } while (0)
+
+#define CKL(what)                                         \
+  do {                                                    \
+    ++launches;                                           \
+    cudaError_t e_ = cudaGetLastError();                  \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what);    \
+  } while (0)
+
+static PFN_cuTensorMapEncodeTiled_v12000 oz_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// digits [kOzS][rows][kpad] int8 as a 3-D tensor; box {kOzBK, box_rows, kOzS}
+static int oz_encode(CUtensorMap* m, void* base, int kpad, int rows, int box_rows) {
+  auto enc = oz_encoder();
+  if (!enc) return 1;
+  const cuuint64_t dims[3] = {(cuuint64_t)kpad, (cuuint64_t)rows, (cuuint64_t)kOzS};
+  const cuuint64_t strides[2] = {(cuuint64_t)kpad, (cuuint64_t)kpad * (cuuint64_t)rows};
+  const cuuint32_t box[3] = {(cuuint32_t)kOzBK, (cuuint32_t)box_rows, (cuuint32_t)kOzS};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+             ? 0
+             : 2;
+}
+
+bool Engine::ozaki_enabled() const {
+  const char* e = getenv("BNBG_OZAKI");
+  return e && e[0] == '1';
+}
+
+// side 0: NN (A = X rows, K = p), side 1: TN (A = X columns, K = n)
+int Engine::ozaki_prepare_x(int side) {
+  OzSide& S = oz_[side];
+  if (S.dX) return 0;
+  const int rows = side ? p : n, K = side ? n : p;
+  S.kpad = (K + 15) / 16 * 16;
+  CK(cudaFuncSetAttribute(k_ozaki_gemm<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          kOzSmemBytes));
+  CK(cudaFuncSetAttribute(k_ozaki_gemm<EPI_DERIV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          kOzSmemBytes));
+  CK(cudaMallocAsync(&S.dX, (size_t)kOzS * rows * S.kpad, stream_));
+  CK(cudaMallocAsync(&S.dEx, sizeof(int) * rows, stream_));
+  CK(cudaMallocAsync(&S.dTm, 2 * sizeof(CUtensorMap), stream_));
+  // NN reads X rows with stride n (once per engine); TN reads X columns
+  k_oz_split_rows<<<rows, 256, 0, stream_>>>(dX_, side ? n : 1, side ? 1 : n, nullptr, rows,
+                                             nullptr, K, S.kpad, rows,
+                                             static_cast<signed char*>(S.dX), S.dEx);
+  CKL("k_oz_split_rows(X)");
+  CUtensorMap tm;
+  if (oz_encode(&tm, S.dX, S.kpad, rows, kOzBM)) return fail(4, "ozaki: tensor map (X digits)");
+  CK(cudaMemcpyAsync(S.dTm, &tm, sizeof(tm), cudaMemcpyHostToDevice, stream_));
+  CK(cudaStreamSynchronize(stream_));
+  return 0;
+}
+
+int Engine::ozaki_reserve_b(int side, int m) {
+  OzSide& S = oz_[side];
+  if (m <= S.bcap) return 0;
+  const int cap = std::max(m, std::max(64, 2 * S.bcap));
+  dfree(S.dB);
+  dfree(S.dEb);
+  CK(cudaMallocAsync(&S.dB, (size_t)kOzS * cap * S.kpad, stream_));
+  CK(cudaMallocAsync(&S.dEb, sizeof(int) * cap, stream_));
+  CUtensorMap tm;
+  if (oz_encode(&tm, S.dB, S.kpad, cap, kOzBN)) return fail(4, "ozaki: tensor map (batch digits)");
+  CK(cudaMemcpyAsync(static_cast<char*>(S.dTm) + sizeof(CUtensorMap), &tm, sizeof(tm),
+                     cudaMemcpyHostToDevice, stream_));
+  CK(cudaStreamSynchronize(stream_));
+  S.bcap = cap;
+  return 0;
+}
+
+// C (+ split*split_stride) column act[c] (ldc) = op(X) * Bsrc[:, act[c]] for
+// the ma active columns (Bsrc column c at Bsrc + act[c]*ldb; act nullptr:
+// identity); deriv applies l' (NN: R = l'(X V)).  *nsplit receives the
+// K-split count (TN; NN is never split, its epilogue needs whole sums).
+int Engine::gemm_ozaki(bool tn, bool deriv, const double* Bsrc, int ldb, const int* act, int ma,
+                       const int* d_ncols, double* C, int ldc, long long split_stride,
+                       int* nsplit) {
+  const int side = tn ? 1 : 0;
+  if (int rc = ozaki_prepare_x(side)) return rc;
+  if (int rc = ozaki_reserve_b(side, ma)) return rc;
+  OzSide& S = oz_[side];
+  const int M = tn ? p : n, K = tn ? n : p;
+  k_oz_split_rows<<<ma, 256, 0, stream_>>>(Bsrc, ldb, 1, act, ma, d_ncols, K, S.kpad, S.bcap,
+                                           static_cast<signed char*>(S.dB), S.dEb);
+  CKL("k_oz_split_rows(batch)");
+  const int mt = (M + kOzBM - 1) / kOzBM, nt = (ma + kOzBN - 1) / kOzBN;
+  const int nkb = (K + kOzBK - 1) / kOzBK;
+  int ns = 1;  // TN: one CTA per SM, split K until the tiles cover the SMs
+  while (tn && ns < nsplit_max_ && mt * nt * ns < sms_ && nkb >= 2 * ns * 8) ns *= 2;
+  OzArgs a{};
+  a.tmA = S.dTm;
+  a.tmB = static_cast<const char*>(S.dTm) + sizeof(CUtensorMap);
+  a.ea = S.dEx;
+  a.eb = S.dEb;
+  a.M = M;
+  a.K = K;
+  a.ksplit = ((nkb + ns - 1) / ns) * kOzBK;
+  ns = (K + a.ksplit - 1) / a.ksplit;
+  a.d_ncols = d_ncols;
+  a.act = act;
+  a.C = C;
+  a.ldc = ldc;
+  a.split_stride = split_stride;
+  a.y = dy_;
+  a.loss = loss;
+  if (!deriv)
+    k_ozaki_gemm<EPI_STORE><<<dim3(mt, nt, ns), kOzThreads, kOzSmemBytes, stream_>>>(a);
+  else
+    k_ozaki_gemm<EPI_DERIV><<<dim3(mt, nt, ns), kOzThreads, kOzSmemBytes, stream_>>>(a);
+  CKL("k_ozaki_gemm");
+  if (nsplit) *nsplit = ns;
+  return 0;
+}
+
+}  // namespace bnbg

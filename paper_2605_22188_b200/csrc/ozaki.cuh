@@ -1,0 +1,300 @@
+// ozaki.cuh -- the FP64 contraction of the relaxation emulated on the
+// 5th-generation tensor cores (tcgen05.mma kind::i8, accumulators in TMEM).
+//
+// Ozaki-style splitting with exact integer products:
+//   every row r of A (and column c of B) is scaled by a power of two 2^e_r so
+//   that |x| < 2^e_r, then cut into kOzS signed 8-bit digits
+//       x = 2^e_r * sum_t d_t 2^(-6-7t) + rho,  |d_t| <= 64,  |rho| <= 2^(e_r-56)
+//   (d_0 = rint(64 x'), each later digit the rint of the remainder times 128;
+//   every remainder is exact in FP64).  Then
+//       sum_k A[r,k] B[c,k] ~= 2^(e_r+e_c) sum_D 2^(-12-7D) C_D,
+//       C_D = sum_{t+u=D} sum_k d^A_t[r,k] d^B_u[c,k]   (int32, exact),
+//   keeping the diagonals D = t+u <= kOzS-1.  |C_D| <= kOzS * K * 64^2 < 2^31
+//   for K <= 65 000, so the integer part is exact; the only rounding is the
+//   FP64 recombination (small diagonals first) and the dropped tail
+//   (~2^-55 of max|A_r| max|B_c| per product term).
+//
+// Kernel layout (one 128 x 64 output tile per CTA, K split over blockIdx.z):
+//   warp 0 / lane 0: TMA producer -- per 64-byte K block one 3-D box of all
+//       kOzS A slices {64 B, 128 rows, kOzS} and one of the B slices
+//       {64 B, 64 columns, kOzS}, SWIZZLE_64B (the UMMA K-major canonical
+//       layout), two stages on full/empty mbarriers;
+//   warp 1 / lane 0: MMA issuer -- for every digit pair (t, u) with
+//       t + u = D <= kOzS-1, two K = 32 tcgen05.mma into TMEM accumulator D
+//       (kOzS accumulators x 64 int32 columns = 512 TMEM columns), then
+//       tcgen05.commit to the stage's empty barrier;
+//   all 4 warps: epilogue -- tcgen05.ld of the kOzS accumulators of their 32
+//       TMEM lanes (rows), FP64 recombination, scale, store into the split's
+//       slab (the consumers sum the slabs in order, as for the DMMA kernels).
+#pragma once
+#include <cstdint>
+
+#include "gemm.cuh"  // EPI_STORE / EPI_DERIV, d_loss_deriv
+
+namespace bnbg {
+
+constexpr int kOzS = 8;           // digits per operand: 6 + 7*7 = 55 bits
+constexpr int kOzBM = 128;        // UMMA M (rows of A per CTA)
+constexpr int kOzBN = 64;         // UMMA N (columns of B per CTA)
+constexpr int kOzBK = 64;         // K bytes per stage (SWIZZLE_64B row)
+constexpr int kOzStages = 2;
+constexpr int kOzThreads = 128;
+constexpr int kOzASlab = kOzBM * kOzBK;  // 8 KB per digit
+constexpr int kOzBSlab = kOzBN * kOzBK;  // 4 KB per digit
+constexpr int kOzAStage = kOzS * kOzASlab;
+constexpr int kOzStageBytes = kOzAStage + kOzS * kOzBSlab;
+constexpr int kOzSmemBytes = kOzStages * kOzStageBytes + 1024;  // + alignment slack
+constexpr int kOzTmemCols = 512;
+static_assert(kOzS * kOzBN <= kOzTmemCols, "accumulators fit TMEM");
+static_assert(kOzASlab % 1024 == 0 && kOzBSlab % 1024 == 0 && kOzStageBytes % 1024 == 0,
+              "swizzle atoms 1024-byte aligned");
+
+struct OzArgs {
+  const void* tmA;   // CUtensorMap (global): A digits int8 {Kpad, M rows, kOzS}
+  const void* tmB;   // CUtensorMap (global): B digits int8 {Kpad, Ncap cols, kOzS}
+  const int* ea;     // per A row exponent
+  const int* eb;     // per compact B column exponent
+  int M, K;          // output rows, reduction length
+  int ksplit;        // K per split (multiple of kOzBK)
+  const int* d_ncols;  // active columns (device)
+  const int* act;      // compact -> physical output column (nullptr: identity)
+  double* C;
+  int ldc;
+  long long split_stride;
+  // EPI_DERIV epilogue (NN: R = l'(X V), losses.hpp:65-69): y and the loss
+  const double* y;
+  int loss;
+};
+
+__device__ __forceinline__ unsigned oz_smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void oz_bar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(oz_smem_u32(b)), "r"(count));
+}
+
+__device__ __forceinline__ void oz_bar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "OZ_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra OZ_WAIT_%=;\n"
+      "}\n" ::"r"(oz_smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void oz_tma_3d(void* dst, const void* tmap, int c0, int c1, int c2,
+                                          unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(oz_smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(oz_smem_u32(bar))
+      : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_64B (rows of 64 bytes,
+// 8-row atoms 512 bytes apart), sm_100 version 1.
+__device__ __forceinline__ unsigned long long oz_desc(const void* p) {
+  const unsigned long long addr = oz_smem_u32(p);
+  unsigned long long d = 0;
+  d |= (addr & 0x3FFFFull) >> 4;          // start address
+  d |= 1ull << 16;                         // leading byte offset (unused, swizzled K-major)
+  d |= (512ull >> 4) << 32;                // stride byte offset: 8 rows x 64 B
+  d |= 1ull << 46;                         // version (sm_100)
+  d |= 4ull << 61;                         // layout: SWIZZLE_64B
+  return d;
+}
+
+// instruction descriptor: kind::i8, D s32, A/B signed, both K-major, M=128, N=64
+constexpr unsigned kOzIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(kOzBN >> 3) << 17) |
+                              ((unsigned)(kOzBM >> 4) << 24);
+
+__device__ __forceinline__ void oz_mma(unsigned tmem_d, unsigned long long da,
+                                       unsigned long long db, unsigned accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kOzIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void oz_commit(unsigned long long* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   oz_smem_u32(bar))
+               : "memory");
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kOzThreads, 1) k_ozaki_gemm(const __grid_constant__ OzArgs a) {
+  extern __shared__ __align__(1024) unsigned char oz_raw[];
+  __shared__ __align__(8) unsigned long long full_bar[kOzStages], empty_bar[kOzStages], done_bar;
+  __shared__ unsigned tmem_base_s;
+  const int ncols = *a.d_ncols;
+  const int n0 = blockIdx.y * kOzBN;
+  if (n0 >= ncols) return;
+  const int m0 = blockIdx.x * kOzBM;
+  const int split = blockIdx.z;
+  const int kbeg = split * a.ksplit;
+  const int kend = min(a.K, kbeg + a.ksplit);
+  const int nkb = (kend - kbeg + kOzBK - 1) / kOzBK;
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(oz_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0) {  // TMEM: 512 columns (kOzS accumulators of 64 int32 columns)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     oz_smem_u32(&tmem_base_s)),
+                 "n"(kOzTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < kOzStages; ++s) {
+      oz_bar_init(&full_bar[s], 1);
+      oz_bar_init(&empty_bar[s], 1);
+    }
+    oz_bar_init(&done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const unsigned tmem = tmem_base_s;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer ----
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kOzStages, u = kb / kOzStages;
+      if (u > 0) oz_bar_wait(&empty_bar[s], (u - 1) & 1);  // MMAs of the last use done
+      unsigned char* st = sm + s * kOzStageBytes;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       oz_smem_u32(&full_bar[s])),
+                   "r"((unsigned)kOzStageBytes)
+                   : "memory");
+      const int k0 = kbeg + kb * kOzBK;
+      oz_tma_3d(st, a.tmA, k0, m0, 0, &full_bar[s]);
+      oz_tma_3d(st + kOzAStage, a.tmB, k0, n0, 0, &full_bar[s]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer ----
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kOzStages, u = kb / kOzStages;
+      oz_bar_wait(&full_bar[s], u & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const unsigned char* sa = sm + s * kOzStageBytes;
+      const unsigned char* sb = sa + kOzAStage;
+#pragma unroll 1
+      for (int D = 0; D < kOzS; ++D) {
+#pragma unroll 1
+        for (int t = 0; t <= D; ++t) {
+          const int ub = D - t;
+#pragma unroll
+          for (int ks = 0; ks < kOzBK / 32; ++ks) {
+            const unsigned long long da = oz_desc(sa + t * kOzASlab + ks * 32);
+            const unsigned long long db = oz_desc(sb + ub * kOzBSlab + ks * 32);
+            oz_mma(tmem + D * kOzBN, da, db, (kb > 0 || t > 0 || ks > 0) ? 1u : 0u);
+          }
+        }
+      }
+      oz_commit(&empty_bar[s]);  // frees the stage once these MMAs complete
+    }
+    oz_commit(&done_bar);
+  }
+
+  // ---- epilogue: all warps; warp w owns TMEM lanes (rows) 32w .. 32w+31 ----
+  __syncwarp();  // lanes 1..31 of the producer / issuer warps park here, not spinning
+  oz_bar_wait(&done_bar, 0);
+  __syncwarp();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int row = m0 + warp * 32 + lane;
+  const bool row_ok = row < a.M;
+  const int er = row_ok ? a.ea[row] : 0;
+  const double yv = (EPI == EPI_DERIV && row_ok) ? a.y[row] : 0.0;
+  double* Cs = a.C + (size_t)split * a.split_stride;
+#pragma unroll 1
+  for (int cc = 0; cc < kOzBN / 16; ++cc) {
+    double acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+#pragma unroll 1
+    for (int D = kOzS - 1; D >= 0; --D) {  // smallest weights first
+      unsigned v[16];
+      const unsigned taddr = tmem + ((unsigned)(warp * 32) << 16) + D * kOzBN + cc * 16;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+          "%11, %12, %13, %14, %15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+            "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      const double w = ldexp(1.0, -12 - 7 * D);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[i] += (double)(int)v[i] * w;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int c = n0 + cc * 16 + i;
+      if (row_ok && c < ncols) {
+        const int col = a.act ? a.act[c] : c;
+        const double s = ldexp(acc[i], er + a.eb[c]);
+        Cs[(size_t)col * a.ldc + row] = EPI == EPI_DERIV ? d_loss_deriv(a.loss, s, yv) : s;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(kOzTmemCols));
+}
+
+// Digits of rows of a matrix: row r (physical rows[r] when rows != nullptr)
+// has elements src[phys*ld_r + k*ld_k], k < K.  out[t][r][k] (row stride
+// Kpad, digit stride Mpad*Kpad), zero for k in [K, Kpad); exps[r].
+// One CTA per row.
+__global__ void k_oz_split_rows(const double* __restrict__ src, long long ld_r, long long ld_k,
+                                const int* rows, int nrows, const int* d_nrows, int K, int Kpad,
+                                long long Mpad, signed char* __restrict__ out,
+                                int* __restrict__ exps) {
+  const int r = blockIdx.x;
+  const int nr = d_nrows ? *d_nrows : nrows;
+  if (r >= nr) return;
+  const long long phys = rows ? rows[r] : r;
+  const double* x = src + phys * ld_r;
+  __shared__ double red[32];
+  double mx = 0.0;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) mx = fmax(mx, fabs(x[(long long)k * ld_k]));
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    mx = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (threadIdx.x == 0) red[0] = mx;
+  }
+  __syncthreads();
+  mx = red[0];
+  int e = 0;
+  if (mx > 0.0) {
+    frexp(mx, &e);  // mx = f * 2^e, f in [0.5, 1): |x| < 2^e
+  }
+  if (threadIdx.x == 0) exps[r] = e;
+  const size_t slab = (size_t)Mpad * Kpad;
+  signed char* o = out + (size_t)r * Kpad;
+  for (int k = threadIdx.x; k < Kpad; k += blockDim.x) {
+    double y = k < K ? ldexp(x[(long long)k * ld_k], 6 - e) : 0.0;  // |y| < 64
+#pragma unroll
+    for (int t = 0; t < kOzS; ++t) {
+      const double d = rint(y);
+      o[t * slab + k] = static_cast<signed char>(d);
+      y = (y - d) * 128.0;  // exact: |y - d| <= 1/2
+    }
+  }
+}
+
+}  // namespace bnbg

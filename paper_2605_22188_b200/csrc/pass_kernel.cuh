@@ -114,16 +114,22 @@ __device__ inline int pass_phase_tn(const PassArgs& a, int ma, double* smem, int
   if (pass_big(a, ma)) {
     auto* epi = reinterpret_cast<double(*)[4][kBigBN]>(smem + kBigSmemBytes / sizeof(double));
     const int mt = (a.p + kBigBM - 1) / kBigBM;
-    if (ma >= kBigNarrowMax) {
-      const int nt = (ma + kBigBN - 1) / kBigBN;
-      for (int t = blockIdx.x; t < mt * nt; t += gridDim.x)
-        gemm_big_tile<true, EPI_STORE, 64>(g, ma, t % mt, t / mt, smem, colmap, epi);
-    } else {
-      const int nt = (ma + 31) / 32;
-      for (int t = blockIdx.x; t < mt * nt; t += gridDim.x)
-        gemm_big_tile<true, EPI_STORE, 32>(g, ma, t % mt, t / mt, smem, colmap, epi);
+    const int bn = ma >= kBigNarrowMax ? kBigBN : 32;
+    const int nt = (ma + bn - 1) / bn;
+    // split K until every CTA has a tile (c3: p / 128 = 16 row tiles)
+    const int nkt = (a.n + kBigBK - 1) / kBigBK;
+    int ns = 1;
+    while (ns < kMaxSplit && mt * nt * ns < (int)gridDim.x && nkt >= 2 * ns * 32) ns *= 2;
+    g.ksplit = ((nkt + ns - 1) / ns) * kBigBK;
+    ns = (a.n + g.ksplit - 1) / g.ksplit;
+    for (int t = blockIdx.x; t < mt * nt * ns; t += gridDim.x) {
+      const int i = t % mt, rest = t / mt;
+      if (bn == kBigBN)
+        gemm_big_tile<true, EPI_STORE, 64>(g, ma, i, rest % nt, smem, colmap, epi, rest / nt);
+      else
+        gemm_big_tile<true, EPI_STORE, 32>(g, ma, i, rest % nt, smem, colmap, epi, rest / nt);
     }
-    return 1;
+    return ns;
   }
   const int fn = pass_fn(ma);
   const int mt = (a.p + 15) / 16;
@@ -401,7 +407,7 @@ constexpr int kActCache = 256;
 
 template <int E>
 __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant__ PassArgs a) {
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double smem[];
   __shared__ int colmap[kBigBN];  // column map of the current GEMM tile (<= 64 columns)
   __shared__ int s_act[kActCache];  // the active list, refreshed after every compaction
   const RelaxDev& r = a.r;  // kernel-parameter space (no local copy)
@@ -412,6 +418,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
   long long node_its = 0;
   unsigned bar_target = 0;
   if (res) res_load_x(a, smem);
+  else if (a.nn.tmap) gemm_big_tma_init();
   int ma = 0;
   const int* actp = r.act;
   // CTA c owns active column c between compactions: its B, V, states in

@@ -44,7 +44,7 @@ def host_ops_check():
     dist.destroy_process_group()
 
 
-def solve(transport, n, p, k, rho, loss, seed, batch):
+def solve(transport, n, p, k, rho, loss, seed, batch, time_limit=float("inf")):
     import torch
     import torch.distributed as dist
     import paper_2605_22188_b200 as P
@@ -54,11 +54,18 @@ def solve(transport, n, p, k, rho, loss, seed, batch):
     dist.init_process_group("nccl" if transport == "nccl" else "gloo")
     inst, _ = P.generate_synthetic(P.GeneratorSpec(n=n, p=p, k=k, correlation=rho, loss=loss,
                                                    seed=seed))
-    cfg = P.SolverConfig(batch_size=batch) if batch else P.SolverConfig()
+    cfg = P.SolverConfig(batch_size=batch, time_limit=time_limit)
     with P.Engine(inst, device=dev) as eng:
-        cert = eng.solve_sharded(cfg, transport=transport)
+        try:
+            cert = eng.solve_sharded(cfg, transport=transport)
+        except Exception as e:  # noqa: BLE001 -- reported, every rank must get here
+            emit({"rank": dist.get_rank(), "error": f"{type(e).__name__}: {e}"})
+            return
+        stats = eng.shard_stats()
     emit({"rank": dist.get_rank(), "support": cert.support, "value": cert.optimal_value,
-          "nodes": cert.nodes_processed, "status": cert.status, "lb_batches": cert.lb_batches})
+          "nodes": cert.nodes_processed, "status": cert.status, "lb_batches": cert.lb_batches,
+          "sent": stats["sent"], "received": stats["received"],
+          "batch_per_pass": stats["batch_per_pass"]})
     dist.destroy_process_group()
 
 
@@ -68,4 +75,4 @@ if __name__ == "__main__":
     else:
         a = sys.argv[2:]
         solve(sys.argv[1], int(a[0]), int(a[1]), int(a[2]), float(a[3]), int(a[4]), int(a[5]),
-              int(a[6]) if len(a) > 6 else 0)
+              int(a[6]) if len(a) > 6 else 0, float(a[7]) if len(a) > 7 else float("inf"))

@@ -35,3 +35,43 @@ def test_sharded_nccl_world1(bnb):
     assert d["support"] == ref.support and d["status"] == "optimal"
     assert abs(d["value"] - ref.optimal_value) <= REL * abs(ref.optimal_value)
     assert d["nodes"] == ref.nodes_processed  # one rank: the same search
+
+
+def test_sharded_c3_moves_node_records(bnb):
+    """c3 size (squared n=5000 p=2000 k=10 rho=0.9) on 2 ranks sharing the
+    GPU over the host transport, 8 s limit: >= 100 node records move through
+    pool_pack / exchange / pool_unpack (the skew rule set to rebalance whenever
+    the two queues differ), and both ranks hold the single-GPU
+    incumbent (support {199, ..., 1999}, value of the reference's own search,
+    tests/golden/replay_c3.json)."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "replay_c3.json")) as f:
+        ub = json.load(f)["passes"][0]["ub"]
+    os.environ["BNBG_BALANCE_SKEW"] = "1,0"  # rebalance whenever the queues differ
+    try:
+        res = run_ranks(2, "host", 5000, 2000, 10, 0.9, 0, 0, 0, 8.0)
+    finally:
+        del os.environ["BNBG_BALANCE_SKEW"]
+    moved = sum(d["sent"] for d in res)
+    assert moved == sum(d["received"] for d in res) and moved >= 100, res
+    for d in res:
+        assert d["support"] == list(range(199, 2000, 200))
+        assert abs(d["value"] - ub) <= REL * abs(ub)
+        print(f"rank {d['rank']}: sent {d['sent']} received {d['received']} records; "
+              f"batch per pass {d['batch_per_pass']}")
+    assert all(len(d["batch_per_pass"]) >= 5 for d in res)
+
+
+def test_sharded_error_reaches_every_rank(bnb):
+    """A failure inside one rank's pass (injected: BNBG_FAULT=rank:pass) is
+    carried through the per-pass collectives: every rank returns an error
+    instead of blocking in the next allgather."""
+    import os
+    os.environ["BNBG_FAULT"] = "1:2"
+    try:
+        res = run_ranks(2, "host", 300, 60, 5, 0.8, 0, 2, 4, timeout=300)
+    finally:
+        del os.environ["BNBG_FAULT"]
+    assert all("error" in d for d in res), res
+    assert "injected" in res[1]["error"] and "rank 1" in res[0]["error"]
