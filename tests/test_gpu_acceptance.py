@@ -15,9 +15,11 @@ host I/O) or out of scope (partitioned_eval).  Here:
       (SPEC.md:808);
   #6  Rashomon completeness on 50 enumeration instances, eps = 0.1, uncapped
       and cap N = 5 (SPEC.md:810);
-  #8  batching speedup: n = p = 300, rho = 0.9, k = 8 squared needs >= 2000
-      nodes and certifies at batch 256 in <= 1/3 of the batch-1 time
-      (SPEC.md:812);
+  #8  batching speedup: a squared instance that needs >= 2000 nodes
+      certifies at batch 256 in <= 1/3 of the batch-1 time (the
+      spec's "e.g. n = p = 300" instance needs > 150 000 nodes on this
+      generator, too many for a batch-1 run in a test, so n = 150, p = 80,
+      k = 6, rho = 0.9: ~12 000 nodes);
   #10 profiling coherence: component seconds within 5% of total wall time,
       lb/reopt batch counters present (SPEC.md:814);
   and the packer's Fig. 2 batch.
@@ -51,21 +53,22 @@ def test_acceptance2_safe_bounds_1e5(bnb, enum_instances):
     total, bad = 0, []
     for loss, seed, inst, vals in enum_instances:
         cache = {}
-        for cfg in (bnb.SolverConfig(prune_slack=0.0, batch_size=1,
-                                     relax=bnb.RelaxConfig(check_interval=1)),
-                    bnb.SolverConfig(prune_slack=0.0, relax=bnb.RelaxConfig(check_interval=1))):
-            def on_dual(node, psi):
-                nonlocal total
-                total += 1
-                key = (tuple(sorted(node.fixed_zero)), tuple(sorted(node.fixed_one)))
-                if key not in cache:
-                    cache[key] = node_optimum(vals, *key)
-                opt = cache[key]
-                if psi > opt + 1e-9 * max(1.0, abs(opt)):
-                    bad.append((loss, seed, key, psi, opt))
-
-            cert = bnb.solve(inst, cfg, bnb.DebugHooks(on_dual_bound=on_dual))
-            assert cert.status == "optimal"
+        events = []
+        with bnb.Engine(inst) as eng:
+            for cfg in (bnb.SolverConfig(prune_slack=0.0, batch_size=1,
+                                         relax=bnb.RelaxConfig(check_interval=1)),
+                        bnb.SolverConfig(prune_slack=0.0, relax=bnb.RelaxConfig(check_interval=1))):
+                cert = eng.solve(cfg, bnb.DebugHooks(on_dual_bound=lambda nd, v: events.append(
+                    (tuple(sorted(nd.fixed_zero)), tuple(sorted(nd.fixed_one)), v))))
+                assert cert.status == "optimal"
+        for z, o, psi in events:
+            key = (z, o)
+            if key not in cache:
+                cache[key] = node_optimum(vals, z, o)
+            opt = cache[key]
+            if psi > opt + 1e-9 * max(1.0, abs(opt)):
+                bad.append((loss, seed, key, psi, opt))
+        total += len(events)
     print(f"#2: {total} device lower bounds checked against enumerated node optima")
     assert not bad, bad[:5]
     assert total >= 100_000
@@ -244,9 +247,10 @@ def test_acceptance6_rashomon_50_instances(bnb, enum_instances):
 
 
 def test_acceptance8_batching_speedup(bnb):
-    """#8: n = p = 300, rho = 0.9, k = 8, squared: >= 2000 nodes; batch 256
-    certifies in <= 1/3 of the batch-1 wall time, both at gap 0."""
-    inst, _ = bnb.generate_synthetic(bnb.GeneratorSpec(n=300, p=300, k=8, correlation=0.9,
+    """#8: n = 150, p = 80, k = 6, rho = 0.9, squared (>= 2000 nodes; see the
+    module docstring): batch 256 certifies in <= 1/3 of the batch-1 wall time,
+    both at gap 0 with the same support."""
+    inst, _ = bnb.generate_synthetic(bnb.GeneratorSpec(n=150, p=80, k=6, correlation=0.9,
                                                        loss=0, seed=0))
     with bnb.Engine(inst) as eng:
         eng.solve(bnb.SolverConfig(batch_size=256, time_limit=2.0))  # warm-up
@@ -274,7 +278,7 @@ def test_acceptance10_profiling_coherence(bnb, enum_instances):
     for loss, seed, inst, _ in enum_instances[::10]:
         runs.append(bnb.solve(inst, bnb.SolverConfig(batch_size=1)))
     for n, p, k, rho, loss in [(1000, 100, 5, 0.5, 0), (2000, 500, 8, 0.7, 1),
-                               (300, 300, 8, 0.9, 0)]:
+                               (150, 80, 6, 0.9, 0)]:
         inst, _ = bnb.generate_synthetic(bnb.GeneratorSpec(n=n, p=p, k=k, correlation=rho,
                                                            loss=loss, seed=0))
         runs.append(bnb.solve(inst))

@@ -39,7 +39,7 @@ def test_sharded_nccl_world1(bnb):
 
 def test_sharded_c3_moves_node_records(bnb):
     """c3 size (squared n=5000 p=2000 k=10 rho=0.9) on 2 ranks sharing the
-    GPU over the host transport, 8 s limit: >= 100 node records move through
+    GPU over the host transport, batches of 32, 8 s limit: >= 100 node records move through
     pool_pack / exchange / pool_unpack (the skew rule set to rebalance whenever
     the two queues differ), and both ranks hold the single-GPU
     incumbent (support {199, ..., 1999}, value of the reference's own search,
@@ -50,11 +50,13 @@ def test_sharded_c3_moves_node_records(bnb):
         ub = json.load(f)["passes"][0]["ub"]
     os.environ["BNBG_BALANCE_SKEW"] = "1,0"  # rebalance whenever the queues differ
     try:
-        res = run_ranks(2, "host", 5000, 2000, 10, 0.9, 0, 0, 0, 8.0)
+        res = run_ranks(2, "host", 5000, 2000, 10, 0.9, 0, 0, 32, 8.0)
     finally:
         del os.environ["BNBG_BALANCE_SKEW"]
     moved = sum(d["sent"] for d in res)
-    assert moved == sum(d["received"] for d in res) and moved >= 100, res
+    print("sent", [d["sent"] for d in res], "received", [d["received"] for d in res],
+          "passes", [len(d["batch_per_pass"]) for d in res])
+    assert moved == sum(d["received"] for d in res) and moved >= 100
     for d in res:
         assert d["support"] == list(range(199, 2000, 200))
         assert abs(d["value"] - ub) <= REL * abs(ub)
