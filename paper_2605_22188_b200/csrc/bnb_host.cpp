@@ -300,7 +300,9 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
   // Test instrumentation (BNBG_FAULT="rank:pass"): that rank's pass fails
   // with a numeric error, exercising the error path of the collectives.
   int fault_rank = -1, fault_pass = -1;
+  int64_t rotate = 0;
   if (comm) {
+    if (const char* r = getenv("BNBG_BALANCE_ROTATE")) rotate = std::max(0, atoi(r));
     h->shard_sent = h->shard_recv = 0;
     h->shard_batch.clear();
     if (const char* f = getenv("BNBG_FAULT")) sscanf(f, "%d:%d", &fault_rank, &fault_pass);
@@ -507,8 +509,24 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
         global_open += counts[r] + (int64_t)all[5 * r + 1];
         global_stop = global_stop || all[5 * r + 3] != 0.0;
       }
-      if (global_open > 0 && !global_stop &&
-          bnbg::balance_plan(world, counts.data(), moves.data())) {
+      bool move = global_open > 0 && !global_stop &&
+                  bnbg::balance_plan(world, counts.data(), moves.data());
+      // Test instrumentation (BNBG_BALANCE_ROTATE=k): on top of the plan,
+      // every rank hands min(k, queue / 2) nodes to the next rank each pass,
+      // exercising pool_pack / exchange / pool_unpack on balanced searches.
+      if (rotate > 0 && global_open > 0 && !global_stop && world > 1) {
+        if (!move) std::fill(moves.begin(), moves.end(), 0);
+        for (int r = 0; r < world; ++r) {
+          int64_t left = counts[r];
+          for (int q = 0; q < world; ++q) left -= moves[(size_t)r * world + q];
+          const int64_t t = std::min<int64_t>(rotate, left / 2);
+          if (t > 0) {
+            moves[(size_t)r * world + (r + 1) % world] += t;
+            move = true;
+          }
+        }
+      }
+      if (move) {
         // donors hand over every other node from the top of their queue
         std::vector<int64_t> send_n(world, 0), recv_n(world, 0);
         int64_t nsend = 0, nrecv = 0;

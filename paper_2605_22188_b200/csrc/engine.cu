@@ -432,7 +432,7 @@ Engine::GemmPlan Engine::plan(int Mr, int K, int ncols, bool allow_split) const 
     const int nkt = (K + bk - 1) / bk;
     pl.ksplit = ((nkt + nsplit - 1) / nsplit) * bk;
     pl.nsplit = (K + pl.ksplit - 1) / pl.ksplit;
-    pl.grid = dim3(mt, nt, pl.nsplit);
+    pl.grid = dim3(nt, mt, pl.nsplit);  // column tiles fastest (k_gemm_big)
     return pl;
   }
   pl.fn = ncols <= 8 ? 1 : (ncols <= 16 ? 2 : 4);
@@ -655,7 +655,7 @@ int Engine::evaluate(int ma, double eta, double rho, const RelaxParams& cfg, int
   EvalArgs e;
   e.part_loss = dPL_;
   e.part_conj = dPC_;
-  e.nrb = p1.grid.x;
+  e.nrb = p1.big ? p1.grid.y : p1.grid.x;  // row blocks of the NN partial sums
   e.part_ld = mcap_;
   e.iter = iter;
   e.prune_threshold = thr;

@@ -277,10 +277,12 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_gemm_big(const __grid_consta
   extern __shared__ __align__(128) double smem[];
   __shared__ int colmap[kBigBN];
   __shared__ double epi_red[2][4][kBigBN];  // EVAL: per-warp-row column sums (l, l*)
+  // blockIdx.x walks the column tiles of one row tile, so the CTAs sharing an
+  // X tile run together and all but one read it from L2
   const int ncols = *g.d_ncols;
-  if ((int)blockIdx.y * kBigBN >= ncols) return;
+  if ((int)blockIdx.x * kBigBN >= ncols) return;
   if (g.tmap) gemm_big_tma_init();
-  gemm_big_tile<TN, EPI>(g, ncols, blockIdx.x, blockIdx.y, smem, colmap, epi_red, blockIdx.z);
+  gemm_big_tile<TN, EPI>(g, ncols, blockIdx.y, blockIdx.x, smem, colmap, epi_red, blockIdx.z);
 }
 
 }  // namespace bnbg

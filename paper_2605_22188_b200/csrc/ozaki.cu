@@ -142,9 +142,9 @@ int Engine::gemm_ozaki(bool tn, bool deriv, const double* Bsrc, int ldb, const i
   a.y = dy_;
   a.loss = loss;
   if (!deriv)
-    k_ozaki_gemm<EPI_STORE><<<dim3(mt, nt, ns), kOzThreads, kOzSmemBytes, stream_>>>(a);
+    k_ozaki_gemm<EPI_STORE><<<dim3(nt, mt, ns), kOzThreads, kOzSmemBytes, stream_>>>(a);
   else
-    k_ozaki_gemm<EPI_DERIV><<<dim3(mt, nt, ns), kOzThreads, kOzSmemBytes, stream_>>>(a);
+    k_ozaki_gemm<EPI_DERIV><<<dim3(nt, mt, ns), kOzThreads, kOzSmemBytes, stream_>>>(a);
   CKL("k_ozaki_gemm");
   if (nsplit) *nsplit = ns;
   return 0;

@@ -134,10 +134,12 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_ozaki_gemm(const __grid_const
   extern __shared__ __align__(1024) unsigned char oz_raw[];
   __shared__ __align__(8) unsigned long long full_bar[kOzStages], empty_bar[kOzStages], done_bar;
   __shared__ unsigned tmem_base_s;
+  // blockIdx.x walks the column tiles of one row tile: the CTAs that share
+  // an A (X digits) tile run together and all but the first read it from L2
   const int ncols = *a.d_ncols;
-  const int n0 = blockIdx.y * kOzBN;
+  const int n0 = blockIdx.x * kOzBN;
   if (n0 >= ncols) return;
-  const int m0 = blockIdx.x * kOzBM;
+  const int m0 = blockIdx.y * kOzBM;
   const int split = blockIdx.z;
   const int kbeg = split * a.ksplit;
   const int kend = min(a.K, kbeg + a.ksplit);

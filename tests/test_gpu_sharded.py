@@ -40,19 +40,21 @@ def test_sharded_nccl_world1(bnb):
 def test_sharded_c3_moves_node_records(bnb):
     """c3 size (squared n=5000 p=2000 k=10 rho=0.9) on 2 ranks sharing the
     GPU over the host transport, batches of 32, 8 s limit: >= 100 node records move through
-    pool_pack / exchange / pool_unpack (the skew rule set to rebalance whenever
-    the two queues differ), and both ranks hold the single-GPU
+    pool_pack / exchange / pool_unpack (BNBG_BALANCE_ROTATE=4 moves 4 nodes a
+    pass on top of the balance plan), and both ranks hold the single-GPU
     incumbent (support {199, ..., 1999}, value of the reference's own search,
     tests/golden/replay_c3.json)."""
     import json
     import os
     with open(os.path.join(os.path.dirname(__file__), "golden", "replay_c3.json")) as f:
         ub = json.load(f)["passes"][0]["ub"]
-    os.environ["BNBG_BALANCE_SKEW"] = "1,0"  # rebalance whenever the queues differ
+    # the two searches stay balanced on their own (queues within one node):
+    # additionally rotate 4 nodes a pass to the other rank
+    os.environ["BNBG_BALANCE_ROTATE"] = "4"
     try:
         res = run_ranks(2, "host", 5000, 2000, 10, 0.9, 0, 0, 32, 8.0)
     finally:
-        del os.environ["BNBG_BALANCE_SKEW"]
+        del os.environ["BNBG_BALANCE_ROTATE"]
     moved = sum(d["sent"] for d in res)
     print("sent", [d["sent"] for d in res], "received", [d["received"] for d in res],
           "passes", [len(d["batch_per_pass"]) for d in res])
