@@ -184,12 +184,17 @@ def run_reference(args, spec, rank):
     n, p, k, rho, loss, desc = spec
     O, kind, threads, blas = _cpu_oracle()
     inst = O.generate(n, p, k, rho, loss, 5.0, 0, 2.0, 1.0)
+    def certify(cfg):
+        if args.config == "c5":  # collect_rashomon (rashomon.hpp:149-218)
+            return O.collect_rashomon(inst, cfg, epsilon=0.01)[0]
+        return O.solve(inst, cfg)
+
     for _ in range(args.warmup):  # untimed warm-up: bounded 1 s samples
-        O.solve(inst, O.solver_cfg(workers=threads, time_limit=min(1.0, args.time_limit)))
+        certify(O.solver_cfg(workers=threads, time_limit=min(1.0, args.time_limit)))
     runs = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        c = O.solve(inst, O.solver_cfg(workers=threads, time_limit=args.time_limit))
+        c = certify(O.solver_cfg(workers=threads, time_limit=args.time_limit))
         runs.append((c.nodes_processed, time.perf_counter() - t0, c))
     nodes = sum(r[0] for r in runs)
     secs = sum(r[1] for r in runs)
@@ -225,7 +230,11 @@ def cpu_baseline(config, time_limit):
     n, p, k, rho, loss, desc = CONFIGS[config]
     inst = O.generate(n, p, k, rho, loss, 5.0, 0, 2.0, 1.0)
     t0 = time.perf_counter()
-    c = O.solve(inst, O.solver_cfg(workers=threads, time_limit=time_limit))
+    cfg = O.solver_cfg(workers=threads, time_limit=time_limit)
+    if config == "c5":  # collect_rashomon (rashomon.hpp:149-218), epsilon 0.01
+        c, _pool = O.collect_rashomon(inst, cfg, epsilon=0.01)
+    else:
+        c = O.solve(inst, cfg)
     secs = time.perf_counter() - t0
     return {"value": c.nodes_processed / secs, "unit": "nodes/s", "cores": threads, "kind": kind,
             "sample": (f"one solve of {config}" + ("" if math.isinf(time_limit) else

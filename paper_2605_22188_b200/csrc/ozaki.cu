@@ -70,13 +70,18 @@ int Engine::ozaki_prepare_x(int side) {
   if (S.dX) return 0;
   const int rows = side ? p : n, K = side ? n : p;
   S.kpad = (K + 15) / 16 * 16;
-  CK(cudaFuncSetAttribute(k_ozaki_gemm<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          kOzSmemBytes));
-  CK(cudaFuncSetAttribute(k_ozaki_gemm<EPI_DERIV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          kOzSmemBytes));
+  CK(cudaFuncSetAttribute(k_ozaki_gemm<EPI_STORE, 64>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, OzShape<64>::SmemBytes));
+  CK(cudaFuncSetAttribute(k_ozaki_gemm<EPI_DERIV, 64>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, OzShape<64>::SmemBytes));
+  CK(cudaFuncSetAttribute(k_ozaki_gemm<EPI_STORE, 32>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, OzShape<32>::SmemBytes));
+  CK(cudaFuncSetAttribute(k_ozaki_gemm<EPI_DERIV, 32>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, OzShape<32>::SmemBytes));
   CK(cudaMallocAsync(&S.dX, (size_t)kOzS * rows * S.kpad, stream_));
   CK(cudaMallocAsync(&S.dEx, sizeof(int) * rows, stream_));
-  CK(cudaMallocAsync(&S.dTm, 2 * sizeof(CUtensorMap), stream_));
+  // tensor maps: X digits, batch digits with 64- and 32-column boxes
+  CK(cudaMallocAsync(&S.dTm, 3 * sizeof(CUtensorMap), stream_));
   // NN reads X rows with stride n (once per engine); TN reads X columns
   k_oz_split_rows<<<rows, 256, 0, stream_>>>(dX_, side ? n : 1, side ? 1 : n, nullptr, rows,
                                              nullptr, K, S.kpad, rows,
@@ -97,9 +102,10 @@ int Engine::ozaki_reserve_b(int side, int m) {
   dfree(S.dEb);
   CK(cudaMallocAsync(&S.dB, (size_t)kOzS * cap * S.kpad, stream_));
   CK(cudaMallocAsync(&S.dEb, sizeof(int) * cap, stream_));
-  CUtensorMap tm;
-  if (oz_encode(&tm, S.dB, S.kpad, cap, kOzBN)) return fail(4, "ozaki: tensor map (batch digits)");
-  CK(cudaMemcpyAsync(static_cast<char*>(S.dTm) + sizeof(CUtensorMap), &tm, sizeof(tm),
+  CUtensorMap tm[2];
+  if (oz_encode(&tm[0], S.dB, S.kpad, cap, 64) || oz_encode(&tm[1], S.dB, S.kpad, cap, 32))
+    return fail(4, "ozaki: tensor map (batch digits)");
+  CK(cudaMemcpyAsync(static_cast<char*>(S.dTm) + sizeof(CUtensorMap), tm, sizeof(tm),
                      cudaMemcpyHostToDevice, stream_));
   CK(cudaStreamSynchronize(stream_));
   S.bcap = cap;
@@ -121,13 +127,19 @@ int Engine::gemm_ozaki(bool tn, bool deriv, const double* Bsrc, int ldb, const i
   k_oz_split_rows<<<ma, 256, 0, stream_>>>(Bsrc, ldb, 1, act, ma, d_ncols, K, S.kpad, S.bcap,
                                            static_cast<signed char*>(S.dB), S.dEb);
   CKL("k_oz_split_rows(batch)");
-  const int mt = (M + kOzBM - 1) / kOzBM, nt = (ma + kOzBN - 1) / kOzBN;
+  // one CTA per SM (the digits ring fills shared memory and TMEM).  TN:
+  // 64-column tiles, K split so that the CTAs make about one wave.  NN (no
+  // split: the l' epilogue needs whole sums): 32-column tiles when the
+  // 64-column ones leave a fifth of the SMs idle.
+  const int mt = (M + kOzBM - 1) / kOzBM;
+  const int bn = (!tn && mt * ((ma + 63) / 64) * 5 < 4 * sms_) ? 32 : 64;
+  const int nt = (ma + bn - 1) / bn;
   const int nkb = (K + kOzBK - 1) / kOzBK;
-  int ns = 1;  // TN: one CTA per SM, split K until the tiles cover the SMs
-  while (tn && ns < nsplit_max_ && mt * nt * ns < sms_ && nkb >= 2 * ns * 8) ns *= 2;
+  int ns = 1;
+  if (tn) ns = std::max(1, std::min({nsplit_max_, sms_ / (mt * nt), nkb / 16}));
   OzArgs a{};
   a.tmA = S.dTm;
-  a.tmB = static_cast<const char*>(S.dTm) + sizeof(CUtensorMap);
+  a.tmB = static_cast<const char*>(S.dTm) + (bn == 64 ? 1 : 2) * sizeof(CUtensorMap);
   a.ea = S.dEx;
   a.eb = S.dEb;
   a.M = M;
@@ -141,10 +153,18 @@ int Engine::gemm_ozaki(bool tn, bool deriv, const double* Bsrc, int ldb, const i
   a.split_stride = split_stride;
   a.y = dy_;
   a.loss = loss;
-  if (!deriv)
-    k_ozaki_gemm<EPI_STORE><<<dim3(nt, mt, ns), kOzThreads, kOzSmemBytes, stream_>>>(a);
-  else
-    k_ozaki_gemm<EPI_DERIV><<<dim3(nt, mt, ns), kOzThreads, kOzSmemBytes, stream_>>>(a);
+  const dim3 grid(nt, mt, ns);
+  if (bn == 64) {
+    if (!deriv)
+      k_ozaki_gemm<EPI_STORE, 64><<<grid, kOzThreads, OzShape<64>::SmemBytes, stream_>>>(a);
+    else
+      k_ozaki_gemm<EPI_DERIV, 64><<<grid, kOzThreads, OzShape<64>::SmemBytes, stream_>>>(a);
+  } else {
+    if (!deriv)
+      k_ozaki_gemm<EPI_STORE, 32><<<grid, kOzThreads, OzShape<32>::SmemBytes, stream_>>>(a);
+    else
+      k_ozaki_gemm<EPI_DERIV, 32><<<grid, kOzThreads, OzShape<32>::SmemBytes, stream_>>>(a);
+  }
   CKL("k_ozaki_gemm");
   if (nsplit) *nsplit = ns;
   return 0;

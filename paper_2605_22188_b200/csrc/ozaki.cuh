@@ -35,19 +35,28 @@ namespace bnbg {
 
 constexpr int kOzS = 8;           // digits per operand: 6 + 7*7 = 55 bits
 constexpr int kOzBM = 128;        // UMMA M (rows of A per CTA)
-constexpr int kOzBN = 64;         // UMMA N (columns of B per CTA)
 constexpr int kOzBK = 64;         // K bytes per stage (SWIZZLE_64B row)
 constexpr int kOzStages = 2;
 constexpr int kOzThreads = 128;
 constexpr int kOzASlab = kOzBM * kOzBK;  // 8 KB per digit
-constexpr int kOzBSlab = kOzBN * kOzBK;  // 4 KB per digit
 constexpr int kOzAStage = kOzS * kOzASlab;
-constexpr int kOzStageBytes = kOzAStage + kOzS * kOzBSlab;
-constexpr int kOzSmemBytes = kOzStages * kOzStageBytes + 1024;  // + alignment slack
-constexpr int kOzTmemCols = 512;
-static_assert(kOzS * kOzBN <= kOzTmemCols, "accumulators fit TMEM");
-static_assert(kOzASlab % 1024 == 0 && kOzBSlab % 1024 == 0 && kOzStageBytes % 1024 == 0,
-              "swizzle atoms 1024-byte aligned");
+
+// per column-tile width BN (UMMA N): 64, or 32 when the 64-wide tiles leave
+// SMs idle (narrow batches, NN at c3)
+template <int BN>
+struct OzShape {
+  static constexpr int BSlab = BN * kOzBK;  // 4 / 2 KB per digit
+  static constexpr int StageBytes = kOzAStage + kOzS * BSlab;
+  static constexpr int SmemBytes = kOzStages * StageBytes + 1024;  // + alignment slack
+  static constexpr int TmemCols = kOzS * BN <= 256 ? 256 : 512;    // power of two
+  // instruction descriptor: kind::i8, D s32, A/B signed, both K-major, M=128
+  static constexpr unsigned Idesc = (2u << 4) | (1u << 7) | (1u << 10) |
+                                    ((unsigned)(BN >> 3) << 17) | ((unsigned)(kOzBM >> 4) << 24);
+  static_assert(kOzS * BN <= TmemCols, "accumulators fit TMEM");
+  static_assert(kOzASlab % 1024 == 0 && BSlab % 1024 == 0 && StageBytes % 1024 == 0,
+                "swizzle atoms 1024-byte aligned");
+};
+constexpr int kOzSmemMax = OzShape<64>::SmemBytes;
 
 struct OzArgs {
   const void* tmA;   // CUtensorMap (global): A digits int8 {Kpad, M rows, kOzS}
@@ -108,19 +117,16 @@ __device__ __forceinline__ unsigned long long oz_desc(const void* p) {
   return d;
 }
 
-// instruction descriptor: kind::i8, D s32, A/B signed, both K-major, M=128, N=64
-constexpr unsigned kOzIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(kOzBN >> 3) << 17) |
-                              ((unsigned)(kOzBM >> 4) << 24);
-
 __device__ __forceinline__ void oz_mma(unsigned tmem_d, unsigned long long da,
-                                       unsigned long long db, unsigned accumulate) {
+                                       unsigned long long db, unsigned idesc,
+                                       unsigned accumulate) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(kOzIdesc), "r"(accumulate));
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void oz_commit(unsigned long long* bar) {
@@ -129,15 +135,16 @@ __device__ __forceinline__ void oz_commit(unsigned long long* bar) {
                : "memory");
 }
 
-template <int EPI>
+template <int EPI, int BN>
 __global__ void __launch_bounds__(kOzThreads, 1) k_ozaki_gemm(const __grid_constant__ OzArgs a) {
+  using Sh = OzShape<BN>;
   extern __shared__ __align__(1024) unsigned char oz_raw[];
   __shared__ __align__(8) unsigned long long full_bar[kOzStages], empty_bar[kOzStages], done_bar;
   __shared__ unsigned tmem_base_s;
   // blockIdx.x walks the column tiles of one row tile: the CTAs that share
   // an A (X digits) tile run together and all but the first read it from L2
   const int ncols = *a.d_ncols;
-  const int n0 = blockIdx.x * kOzBN;
+  const int n0 = blockIdx.x * BN;
   if (n0 >= ncols) return;
   const int m0 = blockIdx.y * kOzBM;
   const int split = blockIdx.z;
@@ -148,10 +155,10 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_ozaki_gemm(const __grid_const
       (reinterpret_cast<uintptr_t>(oz_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  if (warp == 0) {  // TMEM: 512 columns (kOzS accumulators of 64 int32 columns)
+  if (warp == 0) {  // TMEM: kOzS accumulators of BN int32 columns
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      oz_smem_u32(&tmem_base_s)),
-                 "n"(kOzTmemCols));
+                 "n"(Sh::TmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (threadIdx.x == 32) {
@@ -172,10 +179,10 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_ozaki_gemm(const __grid_const
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % kOzStages, u = kb / kOzStages;
       if (u > 0) oz_bar_wait(&empty_bar[s], (u - 1) & 1);  // MMAs of the last use done
-      unsigned char* st = sm + s * kOzStageBytes;
+      unsigned char* st = sm + s * Sh::StageBytes;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
                        oz_smem_u32(&full_bar[s])),
-                   "r"((unsigned)kOzStageBytes)
+                   "r"((unsigned)Sh::StageBytes)
                    : "memory");
       const int k0 = kbeg + kb * kOzBK;
       oz_tma_3d(st, a.tmA, k0, m0, 0, &full_bar[s]);
@@ -187,7 +194,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_ozaki_gemm(const __grid_const
       const int s = kb % kOzStages, u = kb / kOzStages;
       oz_bar_wait(&full_bar[s], u & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const unsigned char* sa = sm + s * kOzStageBytes;
+      const unsigned char* sa = sm + s * Sh::StageBytes;
       const unsigned char* sb = sa + kOzAStage;
 #pragma unroll 1
       for (int D = 0; D < kOzS; ++D) {
@@ -197,8 +204,8 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_ozaki_gemm(const __grid_const
 #pragma unroll
           for (int ks = 0; ks < kOzBK / 32; ++ks) {
             const unsigned long long da = oz_desc(sa + t * kOzASlab + ks * 32);
-            const unsigned long long db = oz_desc(sb + ub * kOzBSlab + ks * 32);
-            oz_mma(tmem + D * kOzBN, da, db, (kb > 0 || t > 0 || ks > 0) ? 1u : 0u);
+            const unsigned long long db = oz_desc(sb + ub * Sh::BSlab + ks * 32);
+            oz_mma(tmem + D * BN, da, db, Sh::Idesc, (kb > 0 || t > 0 || ks > 0) ? 1u : 0u);
           }
         }
       }
@@ -218,33 +225,38 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_ozaki_gemm(const __grid_const
   const double yv = (EPI == EPI_DERIV && row_ok) ? a.y[row] : 0.0;
   double* Cs = a.C + (size_t)split * a.split_stride;
 #pragma unroll 1
-  for (int cc = 0; cc < kOzBN / 16; ++cc) {
-    double acc[16];
+  for (int cc = 0; cc < BN / 16; ++cc) {
+    // the kOzS diagonals of this 16-column chunk in flight together, one wait
+    unsigned v[kOzS][16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
-#pragma unroll 1
-    for (int D = kOzS - 1; D >= 0; --D) {  // smallest weights first
-      unsigned v[16];
-      const unsigned taddr = tmem + ((unsigned)(warp * 32) << 16) + D * kOzBN + cc * 16;
+    for (int D = 0; D < kOzS; ++D) {
+      const unsigned taddr = tmem + ((unsigned)(warp * 32) << 16) + D * BN + cc * 16;
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
           "%11, %12, %13, %14, %15}, [%16];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-            "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "=r"(v[D][0]), "=r"(v[D][1]), "=r"(v[D][2]), "=r"(v[D][3]), "=r"(v[D][4]),
+            "=r"(v[D][5]), "=r"(v[D][6]), "=r"(v[D][7]), "=r"(v[D][8]), "=r"(v[D][9]),
+            "=r"(v[D][10]), "=r"(v[D][11]), "=r"(v[D][12]), "=r"(v[D][13]), "=r"(v[D][14]),
+            "=r"(v[D][15])
           : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    double acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+#pragma unroll
+    for (int D = kOzS - 1; D >= 0; --D) {  // smallest weights first
       const double w = ldexp(1.0, -12 - 7 * D);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) acc[i] += (double)(int)v[i] * w;
+      for (int i = 0; i < 16; ++i) acc[i] += (double)(int)v[D][i] * w;
     }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int c = n0 + cc * 16 + i;
       if (row_ok && c < ncols) {
         const int col = a.act ? a.act[c] : c;
-        const double s = ldexp(acc[i], er + a.eb[c]);
-        Cs[(size_t)col * a.ldc + row] = EPI == EPI_DERIV ? d_loss_deriv(a.loss, s, yv) : s;
+        const double sv = ldexp(acc[i], er + a.eb[c]);
+        Cs[(size_t)col * a.ldc + row] = EPI == EPI_DERIV ? d_loss_deriv(a.loss, sv, yv) : sv;
       }
     }
   }
@@ -252,7 +264,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_ozaki_gemm(const __grid_const
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "n"(kOzTmemCols));
+                 "n"(Sh::TmemCols));
 }
 
 // Digits of rows of a matrix: row r (physical rows[r] when rows != nullptr)
