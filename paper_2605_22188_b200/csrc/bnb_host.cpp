@@ -196,30 +196,53 @@ bnbg::RelaxParams relax_params(const bnbg_relax_cfg& c) {
 
 // reoptimize_supports (primal_heuristics.hpp:174-227) is a pure function of
 // each support SEQUENCE (indices in order: the order fixes the summation
-// order of X_S beta), so equal sequences give bit-identical coefficients and
-// objectives.  Deep passes round many nodes to the same sequence; each
-// distinct one is re-optimised once and the results are scattered back.
+// order of X_S beta) for a fixed instance and step, so a sequence's
+// coefficients and objective never change within a solve.  Deep passes round
+// many nodes to the same sequence, and later passes re-round sequences met
+// before: each distinct sequence is re-optimised once per solve (ReoptMemo)
+// and the results are handed out again.
+struct ReoptMemo {
+  static constexpr size_t kMaxEntries = 1 << 19;
+  std::map<std::vector<int>, std::pair<std::vector<double>, double>> done;
+  long long hits = 0;
+};
+
 static int reoptimize_unique(bnbg::Engine& eng, int nsup, const std::vector<int>& off,
-                             const std::vector<int>& idx, double* coef, double* obj) {
-  std::map<std::vector<int>, int> seen;
-  std::vector<int> first(nsup), uoff(1, 0), uidx;
+                             const std::vector<int>& idx, double* coef, double* obj,
+                             ReoptMemo& memo) {
+  std::map<std::vector<int>, int> fresh;  // sequence -> slot in this launch
+  std::vector<int> slot(nsup, -1), uoff(1, 0), uidx;
   for (int s = 0; s < nsup; ++s) {
     std::vector<int> key(idx.begin() + off[s], idx.begin() + off[s + 1]);
-    auto it = seen.find(key);
-    if (it == seen.end()) {
+    auto hit = memo.done.find(key);
+    if (hit != memo.done.end()) {
+      std::copy(hit->second.first.begin(), hit->second.first.end(), coef + off[s]);
+      obj[s] = hit->second.second;
+      ++memo.hits;
+      continue;
+    }
+    auto it = fresh.find(key);
+    if (it == fresh.end()) {
       const int u = (int)uoff.size() - 1;
-      it = seen.emplace(std::move(key), u).first;
+      it = fresh.emplace(std::move(key), u).first;
       uidx.insert(uidx.end(), idx.begin() + off[s], idx.begin() + off[s + 1]);
       uoff.push_back((int)uidx.size());
     }
-    first[s] = it->second;
+    slot[s] = it->second;
   }
   const int nu = (int)uoff.size() - 1;
-  if (nu == nsup) return eng.reoptimize(nsup, off.data(), idx.data(), coef, obj);
+  if (nu == 0) return 0;
   std::vector<double> ucoef(uidx.size() + 1), uobj(nu + 1);
   if (int rc = eng.reoptimize(nu, uoff.data(), uidx.data(), ucoef.data(), uobj.data())) return rc;
+  if (memo.done.size() + fresh.size() > ReoptMemo::kMaxEntries) memo.done.clear();  // bound host memory
+  for (const auto& kv : fresh)
+    memo.done.emplace(kv.first,
+                      std::make_pair(std::vector<double>(ucoef.begin() + uoff[kv.second],
+                                                         ucoef.begin() + uoff[kv.second + 1]),
+                                     uobj[kv.second]));
   for (int s = 0; s < nsup; ++s) {
-    const int u = first[s];
+    const int u = slot[s];
+    if (u < 0) continue;
     std::copy(ucoef.begin() + uoff[u], ucoef.begin() + uoff[u + 1], coef + off[s]);
     obj[s] = uobj[u];
   }
@@ -289,6 +312,7 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
   // non-OK status instead of blocking in the next allgather.
   int pass_rc = 0;
   std::string pass_msg;
+  ReoptMemo memo;  // re-optimised sequences of this solve
   auto fail = [&](int rc, const std::string& msg) -> int {
     if (!comm) return set_err(h, rc, msg);
     if (!pass_rc) {
@@ -402,7 +426,7 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
     std::vector<double> coef(sidx.size() + 1), obj(nsup + 1);
     if (nsup > 0 && !pass_rc) {
       Timer t(cert->reoptimization_seconds);
-      const int rc = reoptimize_unique(eng, nsup, offsets, sidx, coef.data(), obj.data());
+      const int rc = reoptimize_unique(eng, nsup, offsets, sidx, coef.data(), obj.data(), memo);
       if (rc) {
         if (int e = fail(rc, eng.err)) return e;
       }

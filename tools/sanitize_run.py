@@ -6,13 +6,15 @@ compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
   - standalone kernels (BNBG_PERSISTENT=0): narrow split-K GEMMs, prox,
     eval, compaction;
   - the 128 x 64 GEMM with TMA-staged X tiles and split-K TN (m >= 64);
+  - the tcgen05 kind::i8 emulated-FP64 GEMM (BNBG_OZAKI=1), 32- and 64-column
+    tiles, NN with the l' epilogue inside a relaxation;
   - re-opt kernels: cluster (st.async / mbarrier exchange), Gram (squared),
     shared-memory slices (large n);
   - packer, round/select, branch write, node pool, Rashomon;
   - the NaN-key path of the prox (numeric_error) that memcheck flagged in r01.
 
 Usage: compute-sanitizer --tool memcheck python tools/sanitize_run.py [mode]
-mode: all (default) | resident | streaming | standalone | gemm | reopt | errors
+mode: all (default) | resident | streaming | standalone | gemm | ozaki | reopt | errors
 """
 import math
 import os
@@ -52,6 +54,14 @@ def gemm():
             nd.fixed_zero = [b % i.p()]
         res = eng.solve_batch_relaxation(nodes, P.RelaxConfig(max_iterations=30))
         print("wide batch", len(res.bounds), flush=True)
+
+
+def ozaki():
+    os.environ["BNBG_OZAKI"] = "1"
+    try:
+        gemm()
+    finally:
+        os.environ.pop("BNBG_OZAKI")
 
 
 def reopt():
@@ -95,6 +105,8 @@ def main():
         os.environ.pop("BNBG_PERSISTENT")
     if mode in ("all", "gemm"):
         gemm()
+    if mode in ("all", "ozaki"):
+        ozaki()
     if mode in ("all", "reopt"):
         reopt()
     if mode in ("all", "errors"):
