@@ -5,7 +5,7 @@
 // X's digits are cut once per engine (both orientations, on first use);
 // the batch operand's digits every iteration.  The bound evaluation keeps
 // the DMMA kernels (Psi must be exact for the R it is evaluated at,
-// relaxation.hpp:125-147).  BNBG_OZAKI=1 enables the path.
+// relaxation.hpp:125-147).  On by default (BNBG_OZAKI=0 disables).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -59,9 +59,10 @@ static int oz_encode(CUtensorMap* m, void* base, int kpad, int rows, int box_row
              : 2;
 }
 
+// On by default; BNBG_OZAKI=0 keeps every product on the DMMA kernels.
 bool Engine::ozaki_enabled() const {
   const char* e = getenv("BNBG_OZAKI");
-  return e && e[0] == '1';
+  return !(e && e[0] == '0');
 }
 
 // side 0: NN (A = X rows, K = p), side 1: TN (A = X columns, K = n)

@@ -21,17 +21,15 @@ def test_big_gemm_tma_and_split_k(bnb, n, p):
             B = rng.normal(size=(n if trans else p, m))
             cases.append((m, trans, B))
     outs = {}
-    for tma in ("1", "0"):
-        old = os.environ.get("BNBG_TMA")
-        os.environ["BNBG_TMA"] = tma
-        try:
+    os.environ["BNBG_OZAKI"] = "0"  # the DMMA kernels (the emulated path: test_gpu_ozaki.py)
+    try:
+        for tma in ("1", "0"):
+            os.environ["BNBG_TMA"] = tma
             with bnb.Engine(inst) as eng:
                 outs[tma] = [eng.gemm(B, trans) for _, trans, B in cases]
-        finally:
-            if old is None:
-                del os.environ["BNBG_TMA"]
-            else:
-                os.environ["BNBG_TMA"] = old
+    finally:
+        os.environ.pop("BNBG_TMA", None)
+        os.environ.pop("BNBG_OZAKI", None)
     for (m, trans, B), a, b in zip(cases, outs["1"], outs["0"]):
         ref = inst.X.T @ B if trans else inst.X @ B
         assert np.abs(a - ref).max() <= 1e-12 * np.abs(ref).max(), (m, trans)

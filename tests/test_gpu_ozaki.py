@@ -1,5 +1,5 @@
 """The tcgen05 (kind::i8, TMEM) emulated-FP64 TN product G = X' R
-(csrc/ozaki.cuh, BNBG_OZAKI=1): 8 signed 8-bit digits per operand with a
+(csrc/ozaki.cuh; on by default, BNBG_OZAKI=0 disables): 8 signed 8-bit digits per operand with a
 power-of-two scale per row / column, exact int32 digit products on the
 tensor cores, FP64 recombination.  Checked against numpy fp64 and against the
 DMMA kernel: the emulation error bound is ~2^-55 * n * max|x| * max|r| per

@@ -56,8 +56,8 @@ def gemm():
         print("wide batch", len(res.bounds), flush=True)
 
 
-def ozaki():
-    os.environ["BNBG_OZAKI"] = "1"
+def ozaki(flag="1"):
+    os.environ["BNBG_OZAKI"] = flag
     try:
         gemm()
     finally:
@@ -104,7 +104,7 @@ def main():
         solves()
         os.environ.pop("BNBG_PERSISTENT")
     if mode in ("all", "gemm"):
-        gemm()
+        ozaki("0")  # DMMA with TMA-staged tiles
     if mode in ("all", "ozaki"):
         ozaki()
     if mode in ("all", "reopt"):
