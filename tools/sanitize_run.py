@@ -45,7 +45,7 @@ def gemm():
     with P.Engine(i) as eng:
         for m in (64, 130):
             for trans in (False, True):
-                B = rng.normal(size=(i.n if trans else i.p, m))
+                B = rng.normal(size=(i.n() if trans else i.p(), m))
                 ref = i.X.T @ B if trans else i.X @ B
                 out = eng.gemm(B, trans)
                 assert np.abs(out - ref).max() <= 1e-12 * np.abs(ref).max()
