@@ -99,7 +99,6 @@ Engine::~Engine() {
     dfree(S.dEx);
     dfree(S.dB);
     dfree(S.dEb);
-    dfree(S.dTm);
   }
   comm_release();
   for (void* q : pool_mem_) dfree(q);

@@ -175,12 +175,11 @@ class Engine {
   int gemm_ozaki(bool tn, bool deriv, const double* Bsrc, int ldb, const int* act, int ma,
                  const int* d_ncols, double* C, int ldc, long long split_stride, int* nsplit);
   struct OzSide {             // [0] NN (X rows), [1] TN (X columns)
-    void* dX = nullptr;       // X digits [kOzS][rows][kpad] int8
+    void* dX = nullptr;       // X digits, pre-tiled [row tile][K block][digit][128][64 B]
     int* dEx = nullptr;       // per-row exponent
-    void* dB = nullptr;       // batch digits [kOzS][bcap][kpad]
+    void* dB = nullptr;       // batch digits, pre-tiled [col tile][K block][digit][bn][64 B]
     int* dEb = nullptr;
-    void* dTm = nullptr;      // CUtensorMaps: X digits, batch digits
-    int kpad = 0, bcap = 0;
+    int nkb = 0, bcap = 0;    // K blocks (64 B), batch capacity (multiple of 64)
   } oz_[2];
   ResLayout res_{};           // X residency plan (res_.on = 0: streaming)
  public:

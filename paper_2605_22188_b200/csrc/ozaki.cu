@@ -6,9 +6,6 @@
 // the batch operand's digits every iteration.  The bound evaluation keeps
 // the DMMA kernels (Psi must be exact for the R it is evaluated at,
 // relaxation.hpp:125-147).  On by default (BNBG_OZAKI=0 disables).
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
 #include <algorithm>
 #include <cstdlib>
 #include <string>
@@ -31,34 +28,6 @@ namespace bnbg {
     if (e_ != cudaSuccess) return cuda_fail(e_, what);    \
   } while (0)
 
-static PFN_cuTensorMapEncodeTiled_v12000 oz_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q{};
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      f = nullptr;
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-  }();
-  return fn;
-}
-
-// digits [kOzS][rows][kpad] int8 as a 3-D tensor; box {kOzBK, box_rows, kOzS}
-static int oz_encode(CUtensorMap* m, void* base, int kpad, int rows, int box_rows) {
-  auto enc = oz_encoder();
-  if (!enc) return 1;
-  const cuuint64_t dims[3] = {(cuuint64_t)kpad, (cuuint64_t)rows, (cuuint64_t)kOzS};
-  const cuuint64_t strides[2] = {(cuuint64_t)kpad, (cuuint64_t)kpad * (cuuint64_t)rows};
-  const cuuint32_t box[3] = {(cuuint32_t)kOzBK, (cuuint32_t)box_rows, (cuuint32_t)kOzS};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
-             ? 0
-             : 2;
-}
-
 // On by default; BNBG_OZAKI=0 keeps every product on the DMMA kernels.
 bool Engine::ozaki_enabled() const {
   const char* e = getenv("BNBG_OZAKI");
@@ -70,7 +39,8 @@ int Engine::ozaki_prepare_x(int side) {
   OzSide& S = oz_[side];
   if (S.dX) return 0;
   const int rows = side ? p : n, K = side ? n : p;
-  S.kpad = (K + 15) / 16 * 16;
+  S.nkb = (K + kOzBK - 1) / kOzBK;
+  const int rows_pad = (rows + kOzBM - 1) / kOzBM * kOzBM;
   CK(cudaFuncSetAttribute(k_ozaki_gemm<EPI_STORE, 64>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, OzShape<64>::SmemBytes));
   CK(cudaFuncSetAttribute(k_ozaki_gemm<EPI_DERIV, 64>,
@@ -79,36 +49,24 @@ int Engine::ozaki_prepare_x(int side) {
                           cudaFuncAttributeMaxDynamicSharedMemorySize, OzShape<32>::SmemBytes));
   CK(cudaFuncSetAttribute(k_ozaki_gemm<EPI_DERIV, 32>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, OzShape<32>::SmemBytes));
-  CK(cudaMallocAsync(&S.dX, (size_t)kOzS * rows * S.kpad, stream_));
+  CK(cudaMallocAsync(&S.dX, (size_t)kOzS * rows_pad * S.nkb * kOzBK, stream_));
   CK(cudaMallocAsync(&S.dEx, sizeof(int) * rows, stream_));
-  // tensor maps: X digits, batch digits with 64- and 32-column boxes
-  CK(cudaMallocAsync(&S.dTm, 3 * sizeof(CUtensorMap), stream_));
   // NN reads X rows with stride n (once per engine); TN reads X columns
-  k_oz_split_rows<<<rows, 256, 0, stream_>>>(dX_, side ? n : 1, side ? 1 : n, nullptr, rows,
-                                             nullptr, K, S.kpad, rows,
-                                             static_cast<signed char*>(S.dX), S.dEx);
+  k_oz_split_rows<<<rows_pad, 256, 0, stream_>>>(dX_, side ? n : 1, side ? 1 : n, nullptr, rows,
+                                                 nullptr, K, S.nkb, kOzBM,
+                                                 static_cast<signed char*>(S.dX), S.dEx);
   CKL("k_oz_split_rows(X)");
-  CUtensorMap tm;
-  if (oz_encode(&tm, S.dX, S.kpad, rows, kOzBM)) return fail(4, "ozaki: tensor map (X digits)");
-  CK(cudaMemcpyAsync(S.dTm, &tm, sizeof(tm), cudaMemcpyHostToDevice, stream_));
-  CK(cudaStreamSynchronize(stream_));
   return 0;
 }
 
 int Engine::ozaki_reserve_b(int side, int m) {
   OzSide& S = oz_[side];
   if (m <= S.bcap) return 0;
-  const int cap = std::max(m, std::max(64, 2 * S.bcap));
+  const int cap = (std::max(m, std::max(64, 2 * S.bcap)) + 63) / 64 * 64;
   dfree(S.dB);
   dfree(S.dEb);
-  CK(cudaMallocAsync(&S.dB, (size_t)kOzS * cap * S.kpad, stream_));
+  CK(cudaMallocAsync(&S.dB, (size_t)kOzS * cap * S.nkb * kOzBK, stream_));
   CK(cudaMallocAsync(&S.dEb, sizeof(int) * cap, stream_));
-  CUtensorMap tm[2];
-  if (oz_encode(&tm[0], S.dB, S.kpad, cap, 64) || oz_encode(&tm[1], S.dB, S.kpad, cap, 32))
-    return fail(4, "ozaki: tensor map (batch digits)");
-  CK(cudaMemcpyAsync(static_cast<char*>(S.dTm) + sizeof(CUtensorMap), tm, sizeof(tm),
-                     cudaMemcpyHostToDevice, stream_));
-  CK(cudaStreamSynchronize(stream_));
   S.bcap = cap;
   return 0;
 }
@@ -125,9 +83,6 @@ int Engine::gemm_ozaki(bool tn, bool deriv, const double* Bsrc, int ldb, const i
   if (int rc = ozaki_reserve_b(side, ma)) return rc;
   OzSide& S = oz_[side];
   const int M = tn ? p : n, K = tn ? n : p;
-  k_oz_split_rows<<<ma, 256, 0, stream_>>>(Bsrc, ldb, 1, act, ma, d_ncols, K, S.kpad, S.bcap,
-                                           static_cast<signed char*>(S.dB), S.dEb);
-  CKL("k_oz_split_rows(batch)");
   // one CTA per SM (the digits ring fills shared memory and TMEM).  TN:
   // 64-column tiles, K split so that the CTAs make about one wave.  NN (no
   // split: the l' epilogue needs whole sums): 32-column tiles when the
@@ -135,12 +90,17 @@ int Engine::gemm_ozaki(bool tn, bool deriv, const double* Bsrc, int ldb, const i
   const int mt = (M + kOzBM - 1) / kOzBM;
   const int bn = (!tn && mt * ((ma + 63) / 64) * 5 < 4 * sms_) ? 32 : 64;
   const int nt = (ma + bn - 1) / bn;
-  const int nkb = (K + kOzBK - 1) / kOzBK;
+  const int nkb = S.nkb;
+  // the batch digits in the tiling of this launch (bn-row tiles)
+  k_oz_split_rows<<<nt * bn, 256, 0, stream_>>>(Bsrc, ldb, 1, act, ma, d_ncols, K, nkb, bn,
+                                                static_cast<signed char*>(S.dB), S.dEb);
+  CKL("k_oz_split_rows(batch)");
   int ns = 1;
   if (tn) ns = std::max(1, std::min({nsplit_max_, sms_ / (mt * nt), nkb / 16}));
   OzArgs a{};
-  a.tmA = S.dTm;
-  a.tmB = static_cast<const char*>(S.dTm) + (bn == 64 ? 1 : 2) * sizeof(CUtensorMap);
+  a.A = static_cast<const signed char*>(S.dX);
+  a.B = static_cast<const signed char*>(S.dB);
+  a.nkb_total = nkb;
   a.ea = S.dEx;
   a.eb = S.dEb;
   a.M = M;

@@ -15,10 +15,14 @@
 //   (~2^-55 of max|A_r| max|B_c| per product term).
 //
 // Kernel layout (one 128 x 64 output tile per CTA, K split over blockIdx.z):
-//   warp 0 / lane 0: TMA producer -- per 64-byte K block one 3-D box of all
-//       kOzS A slices {64 B, 128 rows, kOzS} and one of the B slices
-//       {64 B, 64 columns, kOzS}, SWIZZLE_64B (the UMMA K-major canonical
-//       layout), two stages on full/empty mbarriers;
+//   warp 0 / lane 0: producer -- per 64-byte K block one 1-D bulk copy
+//       (cp.async.bulk, the TMA engine's linear mode) of the A block and one
+//       of the B block.  The digits are stored pre-tiled in global memory
+//       as [tile][K block][digit][rows][64 B], each 64-byte row already
+//       SWIZZLE_64B-permuted (16-byte chunk c of row r at c ^ ((r >> 1) & 3)),
+//       i.e. exactly the UMMA K-major canonical shared-memory image: one
+//       contiguous 64 KB (A) + 2-4 KB x 8 (B) copy per stage instead of one
+//       TMA request per 64-byte row; two stages on full/empty mbarriers;
 //   warp 1 / lane 0: MMA issuer -- for every digit pair (t, u) with
 //       t + u = D <= kOzS-1, two K = 32 tcgen05.mma into TMEM accumulator D
 //       (kOzS accumulators x 64 int32 columns = 512 TMEM columns), then
@@ -59,8 +63,9 @@ struct OzShape {
 constexpr int kOzSmemMax = OzShape<64>::SmemBytes;
 
 struct OzArgs {
-  const void* tmA;   // CUtensorMap (global): A digits int8 {Kpad, M rows, kOzS}
-  const void* tmB;   // CUtensorMap (global): B digits int8 {Kpad, Ncap cols, kOzS}
+  const signed char* A;  // A digits, pre-tiled: [M tile][K block][digit][128][64 B]
+  const signed char* B;  // B digits, pre-tiled: [N tile][K block][digit][BN][64 B]
+  int nkb_total;         // K blocks per tile row of the layout
   const int* ea;     // per A row exponent
   const int* eb;     // per compact B column exponent
   int M, K;          // output rows, reduction length
@@ -95,13 +100,19 @@ __device__ __forceinline__ void oz_bar_wait(unsigned long long* b, unsigned pari
       : "memory");
 }
 
-__device__ __forceinline__ void oz_tma_3d(void* dst, const void* tmap, int c0, int c1, int c2,
-                                          unsigned long long* bar) {
+__device__ __forceinline__ void oz_bulk(void* dst, const void* src, unsigned bytes,
+                                        unsigned long long* bar) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(oz_smem_u32(dst)),
-      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(oz_smem_u32(bar))
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          oz_smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(oz_smem_u32(bar))
       : "memory");
+}
+
+// byte offset of (row r, byte kk) inside a pre-tiled digit slab of 64-byte
+// rows: the SWIZZLE_64B permutation of the 16-byte chunks
+__host__ __device__ __forceinline__ int oz_swz(int r, int kk) {
+  return r * kOzBK + ((((kk >> 4) ^ (r >> 1)) & 3) << 4) + (kk & 15);
 }
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_64B (rows of 64 bytes,
@@ -184,9 +195,12 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_ozaki_gemm(const __grid_const
                        oz_smem_u32(&full_bar[s])),
                    "r"((unsigned)Sh::StageBytes)
                    : "memory");
-      const int k0 = kbeg + kb * kOzBK;
-      oz_tma_3d(st, a.tmA, k0, m0, 0, &full_bar[s]);
-      oz_tma_3d(st + kOzAStage, a.tmB, k0, n0, 0, &full_bar[s]);
+      const long long kbg = kbeg / kOzBK + kb;  // global K block
+      oz_bulk(st, a.A + ((long long)blockIdx.y * a.nkb_total + kbg) * kOzAStage, kOzAStage,
+              &full_bar[s]);
+      oz_bulk(st + kOzAStage,
+              a.B + ((long long)blockIdx.x * a.nkb_total + kbg) * (kOzS * Sh::BSlab),
+              kOzS * Sh::BSlab, &full_bar[s]);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer ----
@@ -267,22 +281,25 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_ozaki_gemm(const __grid_const
                  "n"(Sh::TmemCols));
 }
 
-// Digits of rows of a matrix: row r (physical rows[r] when rows != nullptr)
-// has elements src[phys*ld_r + k*ld_k], k < K.  out[t][r][k] (row stride
-// Kpad, digit stride Mpad*Kpad), zero for k in [K, Kpad); exps[r].
-// One CTA per row.
+// Digits of rows of a matrix, written pre-tiled and pre-swizzled (the
+// producer's bulk-copy image): row r (physical rows[r] when rows != nullptr)
+// has elements src[phys*ld_r + k*ld_k], k < K; rows are grouped in tiles of
+// tile_rows, K in blocks of kOzBK bytes: out[tile][kb][digit][tile_rows][64 B].
+// Rows r in [nrows, rows_pad) and k in [K, nkb*64) are zero.  exps[r].
+// One CTA per row (rows_pad CTAs).
 __global__ void k_oz_split_rows(const double* __restrict__ src, long long ld_r, long long ld_k,
-                                const int* rows, int nrows, const int* d_nrows, int K, int Kpad,
-                                long long Mpad, signed char* __restrict__ out,
+                                const int* rows, int nrows, const int* d_nrows, int K, int nkb,
+                                int tile_rows, signed char* __restrict__ out,
                                 int* __restrict__ exps) {
   const int r = blockIdx.x;
   const int nr = d_nrows ? *d_nrows : nrows;
-  if (r >= nr) return;
-  const long long phys = rows ? rows[r] : r;
+  const bool live = r < nr;
+  const long long phys = live ? (rows ? rows[r] : r) : 0;
   const double* x = src + phys * ld_r;
   __shared__ double red[32];
   double mx = 0.0;
-  for (int k = threadIdx.x; k < K; k += blockDim.x) mx = fmax(mx, fabs(x[(long long)k * ld_k]));
+  if (live)
+    for (int k = threadIdx.x; k < K; k += blockDim.x) mx = fmax(mx, fabs(x[(long long)k * ld_k]));
   for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
   __syncthreads();
@@ -297,15 +314,17 @@ __global__ void k_oz_split_rows(const double* __restrict__ src, long long ld_r, 
   if (mx > 0.0) {
     frexp(mx, &e);  // mx = f * 2^e, f in [0.5, 1): |x| < 2^e
   }
-  if (threadIdx.x == 0) exps[r] = e;
-  const size_t slab = (size_t)Mpad * Kpad;
-  signed char* o = out + (size_t)r * Kpad;
-  for (int k = threadIdx.x; k < Kpad; k += blockDim.x) {
-    double y = k < K ? ldexp(x[(long long)k * ld_k], 6 - e) : 0.0;  // |y| < 64
+  if (live && threadIdx.x == 0) exps[r] = e;
+  const int tile = r / tile_rows, rr = r % tile_rows;
+  const size_t slab = (size_t)tile_rows * kOzBK;  // one digit of one K block
+  signed char* o = out + (size_t)tile * nkb * kOzS * slab;
+  for (int k = threadIdx.x; k < nkb * kOzBK; k += blockDim.x) {
+    double y = (live && k < K) ? ldexp(x[(long long)k * ld_k], 6 - e) : 0.0;  // |y| < 64
+    signed char* ok = o + (size_t)(k / kOzBK) * kOzS * slab + oz_swz(rr, k % kOzBK);
 #pragma unroll
     for (int t = 0; t < kOzS; ++t) {
       const double d = rint(y);
-      o[t * slab + k] = static_cast<signed char>(d);
+      ok[t * slab] = static_cast<signed char>(d);
       y = (y - d) * 128.0;  // exact: |y - d| <= 1/2
     }
   }

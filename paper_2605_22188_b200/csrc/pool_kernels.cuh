@@ -271,9 +271,11 @@ static __global__ void __launch_bounds__(kPoolThreads)
   }
   const int RI = child_rec_ints(k);
   int* r0 = rec + (size_t)(2 * ps) * RI;
-  for (int q = tid; q < pn1 + 1; q += kPoolThreads) {
-    const int v = q < pn1 ? P.j1[(size_t)par * k + q] : j;
-    if (q < pn1) r0[4 + q] = v;
+  // J1 lists; the unused tail of each k-slot list is -1 (every byte of the
+  // record read back to the host is defined)
+  for (int q = tid; q < k; q += kPoolThreads) {
+    const int v = q < pn1 ? P.j1[(size_t)par * k + q] : (q == pn1 ? j : -1);
+    r0[4 + q] = q < pn1 ? v : -1;
     r0[RI + 4 + q] = v;
   }
 }

@@ -36,6 +36,9 @@ METRICS = {
     "l1tex__t_bytes.sum.per_second": "l1_bytes_per_s",
     "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed":
         "tensor_pipe_elapsed_pct",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pipe_pct",
+    "sm__inst_executed_pipe_tensor_subpipe_imma.avg.pct_of_peak_sustained_active": "imma_pipe_pct",
+    "lts__t_sector_hit_rate.pct": "l2_hit_pct",
 }
 SCALE = {"byte/second": 1, "Kbyte/second": 1e3, "Mbyte/second": 1e6, "Gbyte/second": 1e9,
          "Tbyte/second": 1e12, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Kbyte/block": 1e3,
