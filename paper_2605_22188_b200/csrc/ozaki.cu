@@ -83,12 +83,12 @@ int Engine::gemm_ozaki(bool tn, bool deriv, const double* Bsrc, int ldb, const i
   if (int rc = ozaki_reserve_b(side, ma)) return rc;
   OzSide& S = oz_[side];
   const int M = tn ? p : n, K = tn ? n : p;
-  // one CTA per SM (the digits ring fills shared memory and TMEM).  TN:
-  // 64-column tiles, K split so that the CTAs make about one wave.  NN (no
-  // split: the l' epilogue needs whole sums): 32-column tiles when the
-  // 64-column ones leave a fifth of the SMs idle.
+  // 64-column tiles run one CTA per SM, 32-column tiles two (TMEM and the
+  // ring halve).  TN: 64-column tiles, K split so that the CTAs make about
+  // one wave.  NN (no split: the l' epilogue needs whole sums): 32-column
+  // tiles when the 64-column ones would not fill the SMs.
   const int mt = (M + kOzBM - 1) / kOzBM;
-  const int bn = (!tn && mt * ((ma + 63) / 64) * 5 < 4 * sms_) ? 32 : 64;
+  const int bn = (!tn && mt * ((ma + 63) / 64) < sms_) ? 32 : 64;
   const int nt = (ma + bn - 1) / bn;
   const int nkb = S.nkb;
   // the batch digits in the tiling of this launch (bn-row tiles)
