@@ -83,12 +83,18 @@ int Engine::gemm_ozaki(bool tn, bool deriv, const double* Bsrc, int ldb, const i
   if (int rc = ozaki_reserve_b(side, ma)) return rc;
   OzSide& S = oz_[side];
   const int M = tn ? p : n, K = tn ? n : p;
-  // 64-column tiles run one CTA per SM, 32-column tiles two (TMEM and the
-  // ring halve).  TN: 64-column tiles, K split so that the CTAs make about
-  // one wave.  NN (no split: the l' epilogue needs whole sums): 32-column
-  // tiles when the 64-column ones would not fill the SMs.
+  // one CTA per SM (the digits ring fills shared memory and TMEM).  TN:
+  // 64-column tiles, K split so that the CTAs make about one wave.  NN (no
+  // split: the l' epilogue needs whole sums): the tile width with the fewer
+  // wave-weighted tile costs.
   const int mt = (M + kOzBM - 1) / kOzBM;
-  const int bn = (!tn && mt * ((ma + 63) / 64) < sms_) ? 32 : 64;
+  int bn = 64;
+  if (!tn) {  // waves x per-tile cost (a 32-column tile costs ~0.6 of a 64-column one:
+              // the A digits it loads are the same)
+    const int t64 = mt * ((ma + 63) / 64), t32 = mt * ((ma + 31) / 32);
+    const double c64 = (double)((t64 + sms_ - 1) / sms_), c32 = 0.6 * ((t32 + sms_ - 1) / sms_);
+    if (c32 < c64) bn = 32;
+  }
   const int nt = (ma + bn - 1) / bn;
   const int nkb = S.nkb;
   // the batch digits in the tiling of this launch (bn-row tiles)

@@ -18,15 +18,15 @@
 //   warp 0 / lane 0: producer -- per 64-byte K block one 1-D bulk copy
 //       (cp.async.bulk, the TMA engine's linear mode) of the A block and one
 //       of the B block.  The digits are stored pre-tiled in global memory
-//       as [tile][K block][digit][rows][32 B], each 32-byte row already
-//       SWIZZLE_32B-permuted (16-byte chunk c of row r at c ^ ((r >> 2) & 1)),
+//       as [tile][K block][digit][rows][64 B], each 64-byte row already
+//       SWIZZLE_64B-permuted (16-byte chunk c of row r at c ^ ((r >> 1) & 3)),
 //       i.e. exactly the UMMA K-major canonical shared-memory image: one
-//       contiguous 32 KB (A) + 8 x 1-2 KB (B) copy per stage; a 4-stage (BN
-//       64) or 2-stage (BN 32, two CTAs per SM) ring on full/empty mbarriers;
+//       contiguous 64 KB (A) + 2-4 KB x 8 (B) copy per stage instead of one
+//       TMA request per 64-byte row; two stages on full/empty mbarriers;
 //   warp 1 / lane 0: MMA issuer -- for every digit pair (t, u) with
-//       t + u = D <= kOzS-1, one K = 32 tcgen05.mma into TMEM accumulator D
-//       (kOzS accumulators x BN int32 columns), then tcgen05.commit to the
-//       stage's empty barrier;
+//       t + u = D <= kOzS-1, two K = 32 tcgen05.mma into TMEM accumulator D
+//       (kOzS accumulators x 64 int32 columns = 512 TMEM columns), then
+//       tcgen05.commit to the stage's empty barrier;
 //   all 4 warps: epilogue -- tcgen05.ld of the kOzS accumulators of their 32
 //       TMEM lanes (rows), FP64 recombination, scale, store into the split's
 //       slab (the consumers sum the slabs in order, as for the DMMA kernels).
@@ -39,28 +39,28 @@ namespace bnbg {
 
 constexpr int kOzS = 8;           // digits per operand: 6 + 7*7 = 55 bits
 constexpr int kOzBM = 128;        // UMMA M (rows of A per CTA)
-constexpr int kOzBK = 32;         // K bytes per stage = one UMMA K-step (SWIZZLE_32B row)
+constexpr int kOzBK = 64;         // K bytes per stage (SWIZZLE_64B row)
+constexpr int kOzStages = 2;
 constexpr int kOzThreads = 128;
-constexpr int kOzASlab = kOzBM * kOzBK;  // 4 KB per digit
+constexpr int kOzASlab = kOzBM * kOzBK;  // 8 KB per digit
 constexpr int kOzAStage = kOzS * kOzASlab;
 
-// per column-tile width BN (UMMA N): 64 (4-stage ring, one CTA per SM,
-// 512 TMEM columns), or 32 (2-stage ring, two CTAs per SM sharing TMEM)
+// per column-tile width BN (UMMA N): 64, or 32 when the 64-wide tiles leave
+// SMs idle (narrow batches, NN at c3)
 template <int BN>
 struct OzShape {
-  static constexpr int Stages = BN == 64 ? 4 : 2;  // 2 x (2 x 41 KB) per SM at BN 32
-  static constexpr int BSlab = BN * kOzBK;  // 2 / 1 KB per digit
+  static constexpr int BSlab = BN * kOzBK;  // 4 / 2 KB per digit
   static constexpr int StageBytes = kOzAStage + kOzS * BSlab;
-  static constexpr int SmemBytes = Stages * StageBytes + 1024;  // + alignment slack
+  static constexpr int SmemBytes = kOzStages * StageBytes + 1024;  // + alignment slack
   static constexpr int TmemCols = kOzS * BN <= 256 ? 256 : 512;    // power of two
   // instruction descriptor: kind::i8, D s32, A/B signed, both K-major, M=128
   static constexpr unsigned Idesc = (2u << 4) | (1u << 7) | (1u << 10) |
                                     ((unsigned)(BN >> 3) << 17) | ((unsigned)(kOzBM >> 4) << 24);
   static_assert(kOzS * BN <= TmemCols, "accumulators fit TMEM");
-  static_assert(kOzASlab % 256 == 0 && BSlab % 256 == 0 && StageBytes % 1024 == 0,
-                "swizzle atoms (256 B) aligned");
+  static_assert(kOzASlab % 1024 == 0 && BSlab % 1024 == 0 && StageBytes % 1024 == 0,
+                "swizzle atoms 1024-byte aligned");
 };
-
+constexpr int kOzSmemMax = OzShape<64>::SmemBytes;
 
 struct OzArgs {
   const signed char* A;  // A digits, pre-tiled: [M tile][K block][digit][128][64 B]
@@ -109,23 +109,22 @@ __device__ __forceinline__ void oz_bulk(void* dst, const void* src, unsigned byt
       : "memory");
 }
 
-// byte offset of (row r, byte kk) inside a pre-tiled digit slab of 32-byte
-// rows: the SWIZZLE_32B permutation of the two 16-byte chunks (address bit 4
-// ^= bit 7, i.e. chunk c of row r at c ^ ((r >> 2) & 1))
+// byte offset of (row r, byte kk) inside a pre-tiled digit slab of 64-byte
+// rows: the SWIZZLE_64B permutation of the 16-byte chunks
 __host__ __device__ __forceinline__ int oz_swz(int r, int kk) {
-  return r * kOzBK + ((((kk >> 4) ^ (r >> 2)) & 1) << 4) + (kk & 15);
+  return r * kOzBK + ((((kk >> 4) ^ (r >> 1)) & 3) << 4) + (kk & 15);
 }
 
-// UMMA shared-memory descriptor: K-major, SWIZZLE_32B (rows of 32 bytes,
-// 8-row atoms 256 bytes apart), sm_100 version 1.
+// UMMA shared-memory descriptor: K-major, SWIZZLE_64B (rows of 64 bytes,
+// 8-row atoms 512 bytes apart), sm_100 version 1.
 __device__ __forceinline__ unsigned long long oz_desc(const void* p) {
   const unsigned long long addr = oz_smem_u32(p);
   unsigned long long d = 0;
   d |= (addr & 0x3FFFFull) >> 4;          // start address
   d |= 1ull << 16;                         // leading byte offset (unused, swizzled K-major)
-  d |= (256ull >> 4) << 32;                // stride byte offset: 8 rows x 32 B
+  d |= (512ull >> 4) << 32;                // stride byte offset: 8 rows x 64 B
   d |= 1ull << 46;                         // version (sm_100)
-  d |= 6ull << 61;                         // layout: SWIZZLE_32B
+  d |= 4ull << 61;                         // layout: SWIZZLE_64B
   return d;
 }
 
@@ -148,10 +147,8 @@ __device__ __forceinline__ void oz_commit(unsigned long long* bar) {
 }
 
 template <int EPI, int BN>
-__global__ void __launch_bounds__(kOzThreads, BN == 64 ? 1 : 2)
-    k_ozaki_gemm(const __grid_constant__ OzArgs a) {
+__global__ void __launch_bounds__(kOzThreads, 1) k_ozaki_gemm(const __grid_constant__ OzArgs a) {
   using Sh = OzShape<BN>;
-  constexpr int kOzStages = Sh::Stages;
   extern __shared__ __align__(1024) unsigned char oz_raw[];
   __shared__ __align__(8) unsigned long long full_bar[kOzStages], empty_bar[kOzStages], done_bar;
   __shared__ unsigned tmem_base_s;
@@ -218,9 +215,12 @@ __global__ void __launch_bounds__(kOzThreads, BN == 64 ? 1 : 2)
 #pragma unroll 1
         for (int t = 0; t <= D; ++t) {
           const int ub = D - t;
-          const unsigned long long da = oz_desc(sa + t * kOzASlab);
-          const unsigned long long db = oz_desc(sb + ub * Sh::BSlab);
-          oz_mma(tmem + D * BN, da, db, Sh::Idesc, (kb > 0 || t > 0) ? 1u : 0u);
+#pragma unroll
+          for (int ks = 0; ks < kOzBK / 32; ++ks) {
+            const unsigned long long da = oz_desc(sa + t * kOzASlab + ks * 32);
+            const unsigned long long db = oz_desc(sb + ub * Sh::BSlab + ks * 32);
+            oz_mma(tmem + D * BN, da, db, Sh::Idesc, (kb > 0 || t > 0 || ks > 0) ? 1u : 0u);
+          }
         }
       }
       oz_commit(&empty_bar[s]);  // frees the stage once these MMAs complete
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kOzThreads, BN == 64 ? 1 : 2)
 // Digits of rows of a matrix, written pre-tiled and pre-swizzled (the
 // producer's bulk-copy image): row r (physical rows[r] when rows != nullptr)
 // has elements src[phys*ld_r + k*ld_k], k < K; rows are grouped in tiles of
-// tile_rows, K in blocks of kOzBK bytes: out[tile][kb][digit][tile_rows][32 B].
+// tile_rows, K in blocks of kOzBK bytes: out[tile][kb][digit][tile_rows][64 B].
 // Rows r in [nrows, rows_pad) and k in [K, nkb*64) are zero.  exps[r].
 // One CTA per row (rows_pad CTAs).
 __global__ void k_oz_split_rows(const double* __restrict__ src, long long ld_r, long long ld_k,
