@@ -62,26 +62,27 @@ cudaError_t launch_eval(int E, int m, size_t smem, cudaStream_t st, const RelaxD
 cudaError_t launch_round_select(int E, int m, size_t smem, cudaStream_t st, int p, int n2, int k,
                                 const double* beta, const uint8_t* state, const int* kbar,
                                 const int* one_off, const int* one_idx, const int* one_len, int* sup,
-                                int* len, int* jb) {
+                                int* len, int* jb, double* gscr, long long gstride) {
   DISPATCH_E(E, k_round_select<EV><<<m, kNodeThreads, smem, st>>>(p, n2, k, beta, state, kbar,
                                                                   one_off, one_idx, one_len, sup,
-                                                                  len, jb));
+                                                                  len, jb, gscr, gstride));
   return cudaGetLastError();
 }
 
 cudaError_t launch_prox_standalone(int E, int m, size_t smem, cudaStream_t st, int mode, int p,
                                    int n2, const double* U, const uint8_t* state, const int* kbar,
-                                   double w, double M, double* out) {
+                                   double w, double M, double* out, double* gscr,
+                                   long long gstride) {
   DISPATCH_E(E, k_prox_standalone<EV><<<m, kNodeThreads, smem, st>>>(mode, p, n2, U, state, kbar,
-                                                                     w, M, out));
+                                                                     w, M, out, gscr, gstride));
   return cudaGetLastError();
 }
 
 cudaError_t launch_g_standalone(int E, int m, size_t smem, cudaStream_t st, int mode, int p, int n2,
                                 const double* in, const uint8_t* state, const int* kbar, double M,
-                                double* out) {
+                                double* out, double* gscr, long long gstride) {
   DISPATCH_E(E, k_g_standalone<EV><<<m, kNodeThreads, smem, st>>>(mode, p, n2, in, state, kbar, M,
-                                                                  out));
+                                                                  out, gscr, gstride));
   return cudaGetLastError();
 }
 

@@ -94,6 +94,7 @@ Engine::~Engine() {
   dfree(dPassProf_);
   dfree(dBar_);
   dfree(dTmap_);
+  dfree(dColScr_);
   for (OzSide& S : oz_) {
     dfree(S.dX);
     dfree(S.dEx);
@@ -223,7 +224,14 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
   n2_ = next_pow2(std::max(p, 2));
   colE_ = column_E(n2_);
   csmem_ = column_smem_bytes(p, n2_, colE_);
-  if (csmem_ > 220 * 1024) return fail(1, "p too large for the column kernels");
+  if (csmem_ > 220 * 1024) {
+    // large p (> 7 680): a node's sort keys no longer fit one CTA's shared
+    // memory; the column kernels keep them in a global scratch (L1/L2), one
+    // slice per CTA, and the persistent pass kernel is off (its plan below
+    // fails the shared-memory limit)
+    colstride_ = (long long)((csmem_ + 255) / 256 * 32);  // doubles, 256-byte aligned slices
+    csmem_ = 0;
+  }
   CK(column_set_attrs(colE_, csmem_));
   stamp("attrs");
   // persistent pass kernel: one CTA per SM when it fits (BNBG_PERSISTENT=0
@@ -324,6 +332,10 @@ int Engine::ensure(int m) {
   dfree(dLen_);
   dfree(dJb_);
   const size_t pm = (size_t)p * cap;
+  if (colstride_) {
+    dfree(dColScr_);
+    CK(cudaMallocAsync(&dColScr_, sizeof(double) * (size_t)colstride_ * cap, stream_));
+  }
   CK(cudaMallocAsync(&dB_, sizeof(double) * pm, stream_));
   CK(cudaMallocAsync(&dV_, sizeof(double) * pm, stream_));
   CK(cudaMallocAsync(&dG_, sizeof(double) * pm * nsplit_max_, stream_));
@@ -605,6 +617,8 @@ int Engine::step(int ma, double eta, double rho, const RelaxParams& cfg) {
   r.M = M;
   r.lambda2 = lambda2;
   r.accel = cfg.acceleration;
+  r.colscr = colstride_ ? dColScr_ : nullptr;
+  r.colstride = colstride_;
   tic(KC_PROX);
   ++launches;
   CK(launch_prox_fista(colE_, ma, csmem_, stream_, r));
@@ -651,6 +665,8 @@ int Engine::evaluate(int ma, double eta, double rho, const RelaxParams& cfg, int
   r.M = M;
   r.lambda2 = lambda2;
   r.accel = cfg.acceleration;
+  r.colscr = colstride_ ? dColScr_ : nullptr;
+  r.colstride = colstride_;
   EvalArgs e;
   e.part_loss = dPL_;
   e.part_conj = dPC_;
@@ -709,6 +725,8 @@ int Engine::run_pass(int m, const RelaxParams& cfg, double thr, double eta, doub
   r.M = M;
   r.lambda2 = lambda2;
   r.accel = cfg.acceleration;
+  r.colscr = colstride_ ? dColScr_ : nullptr;
+  r.colstride = colstride_;
   GemmArgs& g1 = a.nn;
   g1.M = n;
   g1.K = p;
@@ -830,7 +848,8 @@ int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_
   if (round_select) {
     ++launches;
     CK(launch_round_select(colE_, m, csmem_, stream_, p, n2_, std::max(k, 1), dB_, dState_, dKbar_,
-                           d_one_off, d_one_idx, d_one_len, dSup_, dLen_, dJb_));
+                           d_one_off, d_one_idx, d_one_len, dSup_, dLen_, dJb_,
+                           colstride_ ? dColScr_ : nullptr, colstride_));
     out.sup.resize((size_t)m * std::max(k, 1));
     out.len.resize(m);
     out.jbranch.resize(m);
@@ -952,7 +971,7 @@ int Engine::round_select(int m, const double* beta, const uint8_t* state, const 
   ++launches;
   CK(launch_round_select(colE_, m, csmem_, stream_, p, n2_, std::max(k, 1), dB_, dState_, dKbar_,
                          one_off ? d_off : nullptr, one_off ? d_idx : nullptr, nullptr, dSup_, dLen_,
-                         dJb_));
+                         dJb_, colstride_ ? dColScr_ : nullptr, colstride_));
   if (sup)
     if (int rc_ = d2h(sup, dSup_, sizeof(int) * (size_t)m * std::max(k, 1))) return rc_;
   if (len) if (int rc_ = d2h(len, dLen_, sizeof(int) * m)) return rc_;
@@ -1168,9 +1187,12 @@ int stateless_column_op(int device, int kind, int mode, int p, int m, const doub
   DevScratch s;
   const int n2 = next_pow2(std::max(p, 2));
   const int E = column_E(n2);
-  const size_t smem = column_smem_bytes(p, n2, E);
-  if (smem > 220 * 1024) return BNBG_INPUT_ERROR;
+  size_t smem = column_smem_bytes(p, n2, E);
+  // large p: column buffers in global memory (see Engine::create)
+  const long long gstride = smem > 220 * 1024 ? (long long)((smem + 255) / 256 * 32) : 0;
+  if (gstride) smem = 0;
   if (e == cudaSuccess) e = column_set_attrs(E, smem);
+  double* gscr = gstride ? s.alloc<double>((size_t)gstride * m, e) : nullptr;
   double* din = s.alloc<double>((size_t)p * m, e);
   uint8_t* dst = s.alloc<uint8_t>((size_t)p * m, e);
   int* dkb = s.alloc<int>(m, e);
@@ -1180,9 +1202,10 @@ int stateless_column_op(int device, int kind, int mode, int p, int m, const doub
   if (e == cudaSuccess) e = cudaMemcpy(dst, state, (size_t)p * m, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(dkb, kbar, sizeof(int) * m, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && kind == 0)
-    e = launch_prox_standalone(E, m, smem, 0, mode, p, n2, din, dst, dkb, w, M, dout);
+    e = launch_prox_standalone(E, m, smem, 0, mode, p, n2, din, dst, dkb, w, M, dout, gscr,
+                               gstride);
   else if (e == cudaSuccess)
-    e = launch_g_standalone(E, m, smem, 0, mode, p, n2, din, dst, dkb, M, dout);
+    e = launch_g_standalone(E, m, smem, 0, mode, p, n2, din, dst, dkb, M, dout, gscr, gstride);
   if (e == cudaSuccess) e = cudaMemcpy(out, dout, sizeof(double) * outn, cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) {
     g_stateless_err = std::string("CUDA error: ") + cudaGetErrorString(e);

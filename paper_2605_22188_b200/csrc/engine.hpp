@@ -216,6 +216,8 @@ class Engine {
   int n2_ = 1;
   int colE_ = 0;        // elements per thread of the register column sort
   size_t csmem_ = 0;    // dynamic shared memory of the column kernels
+  long long colstride_ = 0;     // large p: column buffers in global memory, doubles per CTA
+  double* dColScr_ = nullptr;   // ... mcap_ slices of them
   int sms_ = 148;
   int mcap_ = 0;
   double* dX_ = nullptr;

@@ -66,13 +66,15 @@ cudaError_t launch_eval(int E, int m, size_t smem, cudaStream_t st, const RelaxD
 cudaError_t launch_round_select(int E, int m, size_t smem, cudaStream_t st, int p, int n2, int k,
                                 const double* beta, const uint8_t* state, const int* kbar,
                                 const int* one_off, const int* one_idx, const int* one_len, int* sup,
-                                int* len, int* jb);
+                                int* len, int* jb, double* gscr = nullptr, long long gstride = 0);
+// gscr / gstride: column buffers in global memory (large p), see RelaxDev::colscr
 cudaError_t launch_prox_standalone(int E, int m, size_t smem, cudaStream_t st, int mode, int p,
                                    int n2, const double* U, const uint8_t* state, const int* kbar,
-                                   double w, double M, double* out);
+                                   double w, double M, double* out, double* gscr = nullptr,
+                                   long long gstride = 0);
 cudaError_t launch_g_standalone(int E, int m, size_t smem, cudaStream_t st, int mode, int p, int n2,
                                 const double* in, const uint8_t* state, const int* kbar, double M,
-                                double* out);
+                                double* out, double* gscr = nullptr, long long gstride = 0);
 
 // ---- reopt_kernels.cu ------------------------------------------------------
 // k_reopt_cluster<qmax in {8,16}, rpt>: cs CTAs (one cluster) per support

@@ -62,7 +62,17 @@ struct RelaxDev {
   double eta, rho, M, lambda2;
   int accel;
   unsigned long long* probe;  // optional sub-phase timers of CTA 0's column work (nullptr: off)
+  // large p (column buffers above the shared-memory limit): the column
+  // kernels' key/index/scan buffers live in global memory instead, colstride
+  // doubles per CTA (nullptr: dynamic shared memory)
+  double* colscr;
+  long long colstride;
 };
+
+// the column buffers of CTA blockIdx.x: global scratch (large p) or shared memory
+__device__ __forceinline__ double* col_base(double* gscr, long long gstride, double* sm) {
+  return gscr ? gscr + (size_t)blockIdx.x * gstride : sm;
+}
 
 // CTA 0's sub-phase timer (tools/pass_phases.py); compiled in, off unless r.probe is set
 struct ColProbe {
@@ -659,7 +669,7 @@ template <int E>
 __global__ void __launch_bounds__(kNodeThreads) k_prox_fista(RelaxDev r) {
   extern __shared__ __align__(16) double sm[];
   if ((int)blockIdx.x >= *r.d_ma) return;
-  prox_column<E>(r, r.nsplit, blockIdx.x, sm);
+  prox_column<E>(r, r.nsplit, blockIdx.x, col_base(r.colscr, r.colstride, sm));
 }
 
 // ---------------------------------------------------------------------------
@@ -955,7 +965,7 @@ template <int E>
 __global__ void __launch_bounds__(kNodeThreads) k_eval(RelaxDev r, EvalArgs e) {
   extern __shared__ __align__(16) double sm[];
   if ((int)blockIdx.x >= *r.d_ma) return;
-  eval_column<E>(r, r.nsplit, e, blockIdx.x, sm);
+  eval_column<E>(r, r.nsplit, e, blockIdx.x, col_base(r.colscr, r.colstride, sm));
 }
 
 // order-preserving compaction of the active list by one CTA of NT threads
@@ -1007,10 +1017,10 @@ template <int E>
 __global__ void __launch_bounds__(kNodeThreads)
     k_round_select(int p, int n2, int k, const double* beta, const uint8_t* state, const int* kbar,
                    const int* one_off, const int* one_idx, const int* one_len, int* sup, int* len,
-                   int* jbranch) {
+                   int* jbranch, double* gscr, long long gstride) {
   extern __shared__ __align__(16) double sm[];
   const int b = blockIdx.x;
-  const ColSmem S = col_smem(sm, p, n2, E);
+  const ColSmem S = col_smem(col_base(gscr, gstride, sm), p, n2, E);
   const double* bb = beta + (size_t)b * p;
   const uint8_t* st = state + (size_t)b * p;
   column_sort<kNodeThreads, E>(
@@ -1037,10 +1047,10 @@ __global__ void __launch_bounds__(kNodeThreads)
 template <int E>
 __global__ void __launch_bounds__(kNodeThreads)
     k_prox_standalone(int mode, int p, int n2, const double* U, const uint8_t* state, const int* kbar,
-                      double w, double M, double* out) {
+                      double w, double M, double* out, double* gscr, long long gstride) {
   extern __shared__ __align__(16) double sm[];
   const int b = blockIdx.x;
-  const ColSmem S = col_smem(sm, p, n2, E);
+  const ColSmem S = col_smem(col_base(gscr, gstride, sm), p, n2, E);
   __shared__ double red[kNodeThreads / 32];
   const double* u = U + (size_t)b * p;
   const uint8_t* st = state + (size_t)b * p;
@@ -1084,10 +1094,10 @@ __global__ void __launch_bounds__(kNodeThreads)
 template <int E>
 __global__ void __launch_bounds__(kNodeThreads)
     k_g_standalone(int mode, int p, int n2, const double* in, const uint8_t* state, const int* kbar,
-                   double M, double* out) {
+                   double M, double* out, double* gscr, long long gstride) {
   extern __shared__ __align__(16) double sm[];
   const int b = blockIdx.x;
-  const ColSmem S = col_smem(sm, p, n2, E);
+  const ColSmem S = col_smem(col_base(gscr, gstride, sm), p, n2, E);
   __shared__ double red[kNodeThreads / 32];
   __shared__ int ired[kNodeThreads / 32];
   const double v =
