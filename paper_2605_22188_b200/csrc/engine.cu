@@ -1029,14 +1029,15 @@ int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coe
         break;
       }
     }
-    // Many supports (c4's deep passes): the shared-memory slices run only
-    // sms / cs supports at a time, each on cs SMs; the per-CTA gather form
-    // runs them all at once, reading X_S from L2 (the union of the passes'
-    // columns fits the 126 MB L2) -- about 4x the support-iterations per
-    // SM-second.  BNBG_REOPT_MODE=smem|direct forces one (measurements).
+    // Very many supports: the shared-memory slices run only sms / cs
+    // supports at a time, each on cs SMs; the per-CTA gather form runs them
+    // all at once, reading X_S from L2.  Measured at c4 (30 s runs): gather
+    // form everywhere 7.6 s of re-opt against 5.7 s for the slices, so the
+    // switch is kept for batches of more than 16 waves of clusters.
+    // BNBG_REOPT_MODE=smem|direct forces one (measurements).
     static const char* mode = getenv("BNBG_REOPT_MODE");
     const bool force_smem = mode && mode[0] == 's', force_direct = mode && mode[0] == 'd';
-    if (cs_smem && (force_direct || (!force_smem && nsup > 4 * (sms_ / cs_smem)))) cs_smem = 0;
+    if (cs_smem && (force_direct || (!force_smem && nsup > 16 * (sms_ / cs_smem)))) cs_smem = 0;
   }
   const bool direct = !gram && !cs && !cs_smem && qmax <= 16;
   // the deriv scratch is only used by the generic kernel
