@@ -521,38 +521,27 @@ int Engine::compute_smoothness(double* out) {
     const double nv = vnorm(v);
     for (double& x : v) x /= nv;
   }
-  // X v over column chunks: enough CTAs for the SMs even when n is small
-  const int row_blocks = (n + 255) / 256;
-  int nsplit = std::max(1, std::min(32, (2 * sms_ + row_blocks - 1) / row_blocks));
-  const int chunk = (p + nsplit - 1) / nsplit;
-  nsplit = (p + chunk - 1) / chunk;
-  if (int rc = ensure_aux(sizeof(double) * ((size_t)2 * p + n + 2 + (size_t)nsplit * n + 4)))
-    return rc;
+  if (int rc = ensure_aux(sizeof(double) * ((size_t)2 * p + n + 4))) return rc;
   double* dv = static_cast<double*>(dAux_);
   double* dw = dv + p;
   double* dxv = dw + p;
-  double* dstat = dxv + n;
-  double* dpart = dstat + 2;
-  double* dps = dpart + (size_t)nsplit * n;  // {done, estimate, result, rounds}
+  double* dps = dxv + n;  // {done, estimate, result, rounds}
   if (int rc_ = h2d(dv, v.data(), sizeof(double) * p)) return rc_;
   const double ps0[4] = {0.0, 0.0, -1.0, 0.0};
   if (int rc_ = h2d(dps, ps0, sizeof(ps0))) return rc_;
   // rounds are launched in batches with the stopping test on the device, so
-  // the host synchronises once per batch instead of once per round
+  // the host synchronises once per batch instead of once per round; the
+  // arithmetic is the oracle's sequential order (bit-identical L)
   double ps[4] = {0.0, 0.0, -1.0, 0.0};
   for (int launched = 0; launched < 100;) {
     const int batch = std::min(launched == 0 ? 4 : 8, 100 - launched);
     for (int b = 0; b < batch; ++b) {
-      k_gemv_n_part<<<dim3(row_blocks, nsplit), 256, 0, stream_>>>(n, p, chunk, dX_, dv, dpart, dps);
-      CKL("k_gemv_n_part");
-      k_gemv_n_sum<<<row_blocks, 256, 0, stream_>>>(n, nsplit, dpart, dxv, dps);
-      CKL("k_gemv_n_sum");
-      k_gemv_t<<<(p + 3) / 4, 128, 0, stream_>>>(n, p, dX_, dxv, dw, dps);  // a warp per column
-      CKL("k_gemv_t");
-      k_power_stats<<<1, 256, 0, stream_>>>(p, dv, dw, dstat, dps);
-      CKL("k_power_stats");
-      k_power_update<<<1, 256, 0, stream_>>>(p, dw, dstat, dv, dps);
-      CKL("k_power_update");
+      k_pw_xv<<<(n + 127) / 128, 128, 0, stream_>>>(n, p, dX_, dv, dxv, dps);
+      CKL("k_pw_xv");
+      k_pw_xtv<<<(p + 127) / 128, 128, 0, stream_>>>(n, p, dX_, dxv, dw, dps);
+      CKL("k_pw_xtv");
+      k_pw_step<<<1, 256, 0, stream_>>>(p, dw, dv, dps);
+      CKL("k_pw_step");
     }
     launched += batch;
     if (int rc_ = d2h(ps, dps, sizeof(ps))) return rc_;

@@ -2,7 +2,7 @@
 //
 //   k_reopt / k_reopt_direct / k_reopt_gram   reoptimize_supports
 //                                  (primal_heuristics.hpp:174-227)
-//   k_gemv_n_part / _sum, k_gemv_t, k_power_stats, k_power_update   smoothness_constant
+//   k_pw_xv, k_pw_xtv, k_pw_step     smoothness_constant
 //                                  power iteration (losses.hpp:86-112)
 #pragma once
 #include <cooperative_groups.h>
@@ -746,94 +746,69 @@ static __global__ void __launch_bounds__(kReoptFastThreads)
   if (tid < q) coef_out[off[s] + tid] = bsh[tid];
 }
 
-// --------------------------------------------------------------------------
-// smoothness constant (losses.hpp:86-112): power-iteration GEMVs
-// --------------------------------------------------------------------------
-// X v split over column chunks (grid.y): partial[s*n + i] over chunk s, summed
-// in chunk order by k_gemv_n_sum -- enough CTAs to cover the SMs at c2 sizes
+// smoothness_constant (losses.hpp:86-112), one power-iteration round as
+// three kernels, in EXACTLY the oracle's / the reference's sequential
+// association (oracle.c orc_smoothness; losses.hpp:99-102 evaluated by plain
+// loops): xv_i = sum_j X_ij v_j in j order, w_j = sum_i X_ij xv_i in i order,
+// v.w and |w|^2 in j order, each product rounded before its add (no FMA), so
+// L is bit-identical to the oracle's.
 // ps = {done, estimate, result, rounds}: once `done` is set on the device the
-// remaining kernels of a launched batch of rounds return at once
-static __global__ void k_gemv_n_part(int n, int p, int chunk, const double* __restrict__ X,
-                                     const double* __restrict__ v, double* __restrict__ part,
-                                     const double* ps) {
+// remaining kernels of a launched batch of rounds return at once.
+static __global__ void k_pw_xv(int n, int p, const double* __restrict__ X,
+                               const double* __restrict__ v, double* __restrict__ xv,
+                               const double* ps) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n || ps[0] != 0.0) return;
-  const int j0 = blockIdx.y * chunk, j1 = min(p, j0 + chunk);
   double s = 0.0;
 #pragma unroll 8  // loads issued ahead; the sum keeps its order
-  for (int j = j0; j < j1; ++j) s += X[(size_t)j * n + i] * v[j];
-  part[(size_t)blockIdx.y * n + i] = s;
-}
-
-static __global__ void k_gemv_n_sum(int n, int ns, const double* __restrict__ part,
-                                    double* __restrict__ xv, const double* ps) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || ps[0] != 0.0) return;
-  double s = part[i];
-#pragma unroll 8  // loads issued ahead; the sum keeps its order
-  for (int q = 1; q < ns; ++q) s += part[(size_t)q * n + i];
+  for (int j = 0; j < p; ++j) s = __dadd_rn(s, __dmul_rn(X[(size_t)j * n + i], v[j]));
   xv[i] = s;
 }
 
-
-static __global__ void k_gemv_t(int n, int p, const double* __restrict__ X, const double* __restrict__ xv,
-                         double* __restrict__ w, const double* ps) {
-  const int j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+static __global__ void k_pw_xtv(int n, int p, const double* __restrict__ X,
+                                const double* __restrict__ xv, double* __restrict__ w,
+                                const double* ps) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= p || ps[0] != 0.0) return;
   const double* col = X + (size_t)j * n;
   double s = 0.0;
-#pragma unroll 8  // loads issued ahead; the sum keeps its order
-  for (int i = lane; i < n; i += 32) s += col[i] * xv[i];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) w[j] = s;
+#pragma unroll 8
+  for (int i = 0; i < n; ++i) s = __dadd_rn(s, __dmul_rn(col[i], xv[i]));
+  w[j] = s;
 }
 
-// out[0] = v.w, out[1] = |w|; single CTA of 256 threads
-static __global__ void k_power_stats(int p, const double* v, const double* w, double* out,
-                                     const double* ps) {
-  __shared__ double red[8];
-  if (ps[0] != 0.0) return;
-  double a = 0.0, c = 0.0;
-  for (int j = threadIdx.x; j < p; j += 256) {
-    a += v[j] * w[j];
-    c += w[j] * w[j];
-  }
-  const double dot = block_sum<256>(a, red);
-  const double nrm2 = block_sum<256>(c, red);
-  if (threadIdx.x == 0) {
-    out[0] = dot;
-    out[1] = sqrt(nrm2);
-  }
-}
-
-// one round's host logic of losses.hpp:96-110 on the device (single CTA):
-// stop on a zero or non-positive estimate (result 1e-12), else v = w/|w|, and
-// stop once the estimate changes by at most 1e-4 relative (after round 0)
-static __global__ void k_power_update(int p, const double* w, const double* stat, double* v,
-                                      double* ps) {
+// next = v.w, wn = |w| (sequential), then the round's host logic of
+// losses.hpp:96-110: stop on a zero or non-positive estimate (result 1e-12),
+// else v = w / wn, and stop once the estimate moves by at most 1e-4 relative
+// (after round 0).  One CTA.
+static __global__ void k_pw_step(int p, const double* w, double* v, double* ps) {
   __shared__ int s_dec;
+  __shared__ double s_wn;
   if (ps[0] != 0.0) return;
-  const double next = stat[0], wn = stat[1];
   if (threadIdx.x == 0) {
+    double next = 0.0, nrm2 = 0.0;
+    for (int j = 0; j < p; ++j) next = __dadd_rn(next, __dmul_rn(v[j], w[j]));
+    for (int j = 0; j < p; ++j) nrm2 = __dadd_rn(nrm2, __dmul_rn(w[j], w[j]));
+    const double wn = sqrt(nrm2);
     int dec = 0;  // 0: continue, 1: zero / non-positive, 2: converged
     if (wn == 0.0 || next <= 0.0)
       dec = 1;
     else if (ps[3] > 0.0 && fabs(next - ps[1]) <= 1e-4 * next)
       dec = 2;
-    s_dec = dec;
-  }
-  __syncthreads();
-  const int dec = s_dec;
-  if (dec != 1)
-    for (int j = threadIdx.x; j < p; j += blockDim.x) v[j] = w[j] / wn;
-  if (threadIdx.x == 0) {
     if (dec == 1) {
       ps[2] = 1e-12;
     } else {
       ps[1] = next;
     }
+    s_dec = dec;
+    s_wn = wn;
+  }
+  __syncthreads();
+  const int dec = s_dec;
+  const double wn = s_wn;
+  if (dec != 1)
+    for (int j = threadIdx.x; j < p; j += blockDim.x) v[j] = w[j] / wn;
+  if (threadIdx.x == 0) {
     if (dec != 0) ps[0] = 1.0;
     ps[3] += 1.0;
   }

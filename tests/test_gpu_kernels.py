@@ -138,10 +138,21 @@ def _engine(bnb, orc, n, p, k, rho, loss, seed=0):
     return inst, bnb.Engine(pin)
 
 
+@pytest.mark.parametrize("n,p,k,rho,loss", [(1000, 100, 5, 0.5, 0), (2000, 500, 8, 0.7, 1),
+                                            (30, 12, 3, 0.9, 1), (60, 8200, 2, 0.5, 0),
+                                            (5000, 2000, 10, 0.9, 0)])
+def test_smoothness_bit_identical_to_oracle(bnb, orc, n, p, k, rho, loss):
+    """losses.hpp:86-112 on the device in the oracle's sequential order (no
+    FMA): the smoothness constant -- hence the step 1/L of every relaxation
+    and re-optimisation -- equals oracle.c's bit for bit."""
+    inst, eng = _engine(bnb, orc, n, p, k, rho, loss)
+    assert eng.smoothness() == orc.smoothness(loss, inst.X)
+
+
 def test_smoothness_and_gemm(bnb, orc):
     inst, eng = _engine(bnb, orc, 1000, 100, 5, 0.5, 0)
     L = orc.smoothness(0, inst.X)
-    assert abs(eng.smoothness() - L) <= 1e-12 * L
+    assert eng.smoothness() == L
     rng = np.random.default_rng(3)
     for m in (1, 7, 8, 9, 16, 33, 300):
         for trans in (False, True):
