@@ -53,7 +53,7 @@ int Engine::ozaki_prepare_x(int side) {
   CK(cudaMallocAsync(&S.dEx, sizeof(int) * rows, stream_));
   // NN reads X rows with stride n (once per engine); TN reads X columns
   k_oz_split_rows<<<rows_pad, 256, 0, stream_>>>(dX_, side ? n : 1, side ? 1 : n, nullptr, rows,
-                                                 nullptr, K, S.nkb, kOzBM,
+                                                 nullptr, K, S.nkb, kOzBM, kOzBM,
                                                  static_cast<signed char*>(S.dX), S.dEx);
   CKL("k_oz_split_rows(X)");
   return 0;
@@ -99,7 +99,7 @@ int Engine::gemm_ozaki(bool tn, bool deriv, const double* Bsrc, int ldb, const i
   const int nkb = S.nkb;
   // the batch digits in the tiling of this launch (bn-row tiles)
   k_oz_split_rows<<<nt * bn, 256, 0, stream_>>>(Bsrc, ldb, 1, act, ma, d_ncols, K, nkb, bn,
-                                                static_cast<signed char*>(S.dB), S.dEb);
+                                                kOzG, static_cast<signed char*>(S.dB), S.dEb);
   CKL("k_oz_split_rows(batch)");
   int ns = 1;
   if (tn) ns = std::max(1, std::min({nsplit_max_, sms_ / (mt * nt), nkb / 16}));

@@ -23,10 +23,13 @@
 //       i.e. exactly the UMMA K-major canonical shared-memory image: one
 //       contiguous 64 KB (A) + 2-4 KB x 8 (B) copy per stage instead of one
 //       TMA request per 64-byte row; two stages on full/empty mbarriers;
-//   warp 1 / lane 0: MMA issuer -- for every digit pair (t, u) with
-//       t + u = D <= kOzS-1, two K = 32 tcgen05.mma into TMEM accumulator D
-//       (kOzS accumulators x 64 int32 columns = 512 TMEM columns), then
-//       tcgen05.commit to the stage's empty barrier;
+//   warp 1 / lane 0: MMA issuer -- for each A digit t and 32-column group,
+//       one tcgen05.mma per K = 32 step whose B operand stacks the digits
+//       u = 0 .. kOzS-1-t of the group (N = (kOzS-t)*32 <= 256): product
+//       A_t B_u lands in TMEM column block t+u, the accumulator of its
+//       diagonal (kOzS x 32 int32 columns per group: 512 TMEM columns for
+//       64-column tiles).  8 MMAs of N <= 256 per K-step and group instead of
+//       36 of N = 32; then tcgen05.commit to the stage's empty barrier;
 //   all 4 warps: epilogue -- tcgen05.ld of the kOzS accumulators of their 32
 //       TMEM lanes (rows), FP64 recombination, scale, store into the split's
 //       slab (the consumers sum the slabs in order, as for the DMMA kernels).
@@ -45,17 +48,20 @@ constexpr int kOzThreads = 128;
 constexpr int kOzASlab = kOzBM * kOzBK;  // 8 KB per digit
 constexpr int kOzAStage = kOzS * kOzASlab;
 
-// per column-tile width BN (UMMA N): 64, or 32 when the 64-wide tiles leave
-// SMs idle (narrow batches, NN at c3)
+// B rows are grouped by 32 columns: a group's digit slabs are contiguous,
+// [digit][32 columns][64 B], so B_0 .. B_{S-1} of a group form one operand of
+// up to 256 rows
+constexpr int kOzG = 32;
+constexpr int kOzGSlab = kOzG * kOzBK;  // 2 KB: one digit of one column group
+
+// per column-tile width BN: 64, or 32 when the 64-wide tiles leave SMs idle
+// (narrow batches, NN at c3)
 template <int BN>
 struct OzShape {
   static constexpr int BSlab = BN * kOzBK;  // 4 / 2 KB per digit
   static constexpr int StageBytes = kOzAStage + kOzS * BSlab;
   static constexpr int SmemBytes = kOzStages * StageBytes + 1024;  // + alignment slack
   static constexpr int TmemCols = kOzS * BN <= 256 ? 256 : 512;    // power of two
-  // instruction descriptor: kind::i8, D s32, A/B signed, both K-major, M=128
-  static constexpr unsigned Idesc = (2u << 4) | (1u << 7) | (1u << 10) |
-                                    ((unsigned)(BN >> 3) << 17) | ((unsigned)(kOzBM >> 4) << 24);
   static_assert(kOzS * BN <= TmemCols, "accumulators fit TMEM");
   static_assert(kOzASlab % 1024 == 0 && BSlab % 1024 == 0 && StageBytes % 1024 == 0,
                 "swizzle atoms 1024-byte aligned");
@@ -126,6 +132,12 @@ __device__ __forceinline__ unsigned long long oz_desc(const void* p) {
   d |= 1ull << 46;                         // version (sm_100)
   d |= 4ull << 61;                         // layout: SWIZZLE_64B
   return d;
+}
+
+// instruction descriptor: kind::i8, D s32, A/B signed, both K-major, M = 128, N
+__host__ __device__ __forceinline__ constexpr unsigned oz_idesc(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(n >> 3) << 17) |
+         ((unsigned)(kOzBM >> 4) << 24);
 }
 
 __device__ __forceinline__ void oz_mma(unsigned tmem_d, unsigned long long da,
@@ -210,16 +222,21 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_ozaki_gemm(const __grid_const
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const unsigned char* sa = sm + s * Sh::StageBytes;
       const unsigned char* sb = sa + kOzAStage;
+      // digit-stacked N: for A digit t and a group of 32 columns, ONE MMA
+      // against the B rows (digit u, column c) for u = 0 .. kOzS-1-t (N =
+      // (kOzS-t)*32) lands every product A_t B_u in TMEM column block t+u =
+      // the diagonal D it belongs to (accumulator [group][D][32 columns])
 #pragma unroll 1
-      for (int D = 0; D < kOzS; ++D) {
+      for (int g = 0; g < BN / kOzG; ++g) {
 #pragma unroll 1
-        for (int t = 0; t <= D; ++t) {
-          const int ub = D - t;
+        for (int t = 0; t < kOzS; ++t) {
+          const unsigned idesc = oz_idesc((kOzS - t) * kOzG);
 #pragma unroll
           for (int ks = 0; ks < kOzBK / 32; ++ks) {
             const unsigned long long da = oz_desc(sa + t * kOzASlab + ks * 32);
-            const unsigned long long db = oz_desc(sb + ub * Sh::BSlab + ks * 32);
-            oz_mma(tmem + D * BN, da, db, Sh::Idesc, (kb > 0 || t > 0 || ks > 0) ? 1u : 0u);
+            const unsigned long long db = oz_desc(sb + g * kOzS * kOzGSlab + ks * 32);
+            oz_mma(tmem + g * kOzS * kOzG + t * kOzG, da, db, idesc,
+                   (kb > 0 || t > 0 || ks > 0) ? 1u : 0u);
           }
         }
       }
@@ -244,7 +261,9 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_ozaki_gemm(const __grid_const
     unsigned v[kOzS][16];
 #pragma unroll
     for (int D = 0; D < kOzS; ++D) {
-      const unsigned taddr = tmem + ((unsigned)(warp * 32) << 16) + D * BN + cc * 16;
+      // column block of (group cc*16 / 32, diagonal D), 16-column half of it
+      const unsigned taddr = tmem + ((unsigned)(warp * 32) << 16) +
+                             (cc * 16 / kOzG) * kOzS * kOzG + D * kOzG + (cc * 16) % kOzG;
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
           "%11, %12, %13, %14, %15}, [%16];"
@@ -284,12 +303,14 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_ozaki_gemm(const __grid_const
 // Digits of rows of a matrix, written pre-tiled and pre-swizzled (the
 // producer's bulk-copy image): row r (physical rows[r] when rows != nullptr)
 // has elements src[phys*ld_r + k*ld_k], k < K; rows are grouped in tiles of
-// tile_rows, K in blocks of kOzBK bytes: out[tile][kb][digit][tile_rows][64 B].
+// tile_rows, K in blocks of kOzBK bytes, and inside a tile in groups of
+// group_rows: out[tile][kb][group][digit][group_rows][64 B] (A: one group of
+// 128 rows; B: groups of kOzG columns).
 // Rows r in [nrows, rows_pad) and k in [K, nkb*64) are zero.  exps[r].
 // One CTA per row (rows_pad CTAs).
 __global__ void k_oz_split_rows(const double* __restrict__ src, long long ld_r, long long ld_k,
                                 const int* rows, int nrows, const int* d_nrows, int K, int nkb,
-                                int tile_rows, signed char* __restrict__ out,
+                                int tile_rows, int group_rows, signed char* __restrict__ out,
                                 int* __restrict__ exps) {
   const int r = blockIdx.x;
   const int nr = d_nrows ? *d_nrows : nrows;
@@ -316,11 +337,13 @@ __global__ void k_oz_split_rows(const double* __restrict__ src, long long ld_r, 
   }
   if (live && threadIdx.x == 0) exps[r] = e;
   const int tile = r / tile_rows, rr = r % tile_rows;
-  const size_t slab = (size_t)tile_rows * kOzBK;  // one digit of one K block
-  signed char* o = out + (size_t)tile * nkb * kOzS * slab;
+  const int grp = rr / group_rows, gr = rr % group_rows;
+  const size_t block = (size_t)tile_rows * kOzS * kOzBK;  // one K block of one tile
+  const size_t slab = (size_t)group_rows * kOzBK;         // one digit of one group
+  signed char* o = out + (size_t)tile * nkb * block + (size_t)grp * kOzS * slab;
   for (int k = threadIdx.x; k < nkb * kOzBK; k += blockDim.x) {
     double y = (live && k < K) ? ldexp(x[(long long)k * ld_k], 6 - e) : 0.0;  // |y| < 64
-    signed char* ok = o + (size_t)(k / kOzBK) * kOzS * slab + oz_swz(rr, k % kOzBK);
+    signed char* ok = o + (size_t)(k / kOzBK) * block + oz_swz(gr, k % kOzBK);
 #pragma unroll
     for (int t = 0; t < kOzS; ++t) {
       const double d = rint(y);
