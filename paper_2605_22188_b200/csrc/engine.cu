@@ -536,9 +536,9 @@ int Engine::compute_smoothness(double* out) {
   for (int launched = 0; launched < 100;) {
     const int batch = std::min(launched == 0 ? 4 : 8, 100 - launched);
     for (int b = 0; b < batch; ++b) {
-      k_pw_xv<<<(n + 127) / 128, 128, 0, stream_>>>(n, p, dX_, dv, dxv, dps);
+      k_pw_xv<<<(n + 255) / 256, 256, 0, stream_>>>(n, p, dX_, dv, dxv, dps);
       CKL("k_pw_xv");
-      k_pw_xtv<<<(p + 127) / 128, 128, 0, stream_>>>(n, p, dX_, dxv, dw, dps);
+      k_pw_xtv<<<(p + 7) / 8, 256, 0, stream_>>>(n, p, dX_, dxv, dw, dps);  // a warp per column
       CKL("k_pw_xtv");
       k_pw_step<<<1, 256, 0, stream_>>>(p, dw, dv, dps);
       CKL("k_pw_step");

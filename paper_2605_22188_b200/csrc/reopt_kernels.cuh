@@ -754,27 +754,66 @@ static __global__ void __launch_bounds__(kReoptFastThreads)
 // L is bit-identical to the oracle's.
 // ps = {done, estimate, result, rounds}: once `done` is set on the device the
 // remaining kernels of a launched batch of rounds return at once.
-static __global__ void k_pw_xv(int n, int p, const double* __restrict__ X,
-                               const double* __restrict__ v, double* __restrict__ xv,
-                               const double* ps) {
+// xv = X v, one thread per row, the row's sum in j order.  The row's X
+// elements (coalesced across the warp) and v (a broadcast) are loaded 16
+// columns ahead of the add chain.
+static __global__ void __launch_bounds__(256) k_pw_xv(int n, int p, const double* __restrict__ X,
+                                                      const double* __restrict__ v,
+                                                      double* __restrict__ xv, const double* ps) {
+  if (ps[0] != 0.0) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || ps[0] != 0.0) return;
+  if (i >= n) return;
+  constexpr int U = 16;
+  double bx[U], bv[U];
   double s = 0.0;
-#pragma unroll 8  // loads issued ahead; the sum keeps its order
-  for (int j = 0; j < p; ++j) s = __dadd_rn(s, __dmul_rn(X[(size_t)j * n + i], v[j]));
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    bx[u] = u < p ? X[(size_t)u * n + i] : 0.0;
+    bv[u] = u < p ? __ldg(v + u) : 0.0;
+  }
+  for (int j0 = 0; j0 < p; j0 += U) {
+    double nx[U], nv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + U + u;
+      nx[u] = j < p ? X[(size_t)j * n + i] : 0.0;
+      nv[u] = j < p ? __ldg(v + j) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (j0 + u < p) s = __dadd_rn(s, __dmul_rn(bx[u], bv[u]));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      bx[u] = nx[u];
+      bv[u] = nv[u];
+    }
+  }
   xv[i] = s;
 }
 
-static __global__ void k_pw_xtv(int n, int p, const double* __restrict__ X,
-                                const double* __restrict__ xv, double* __restrict__ w,
-                                const double* ps) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= p || ps[0] != 0.0) return;
+// w = X' xv, one warp per column: the lanes load 32 consecutive rows of the
+// column (coalesced) and form the products; lane 0 adds them in row order.
+static __global__ void __launch_bounds__(256) k_pw_xtv(int n, int p, const double* __restrict__ X,
+                                                       const double* __restrict__ xv,
+                                                       double* __restrict__ w, const double* ps) {
+  if (ps[0] != 0.0) return;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= p) return;
   const double* col = X + (size_t)j * n;
   double s = 0.0;
-#pragma unroll 8
-  for (int i = 0; i < n; ++i) s = __dadd_rn(s, __dmul_rn(col[i], xv[i]));
-  w[j] = s;
+  double prod = lane < n ? __dmul_rn(col[lane], xv[lane]) : 0.0;
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int in = i0 + 32 + lane;  // next chunk's product, ahead of the chain
+    const double nprod = in < n ? __dmul_rn(col[in], xv[in]) : 0.0;
+    const int cnt = min(32, n - i0);
+    for (int q = 0; q < cnt; ++q) {
+      const double t = __shfl_sync(0xffffffffu, prod, q);
+      s = __dadd_rn(s, t);  // lane 0's chain is the one kept
+    }
+    prod = nprod;
+  }
+  if (lane == 0) w[j] = s;
 }
 
 // next = v.w, wn = |w| (sequential), then the round's host logic of
@@ -782,13 +821,32 @@ static __global__ void k_pw_xtv(int n, int p, const double* __restrict__ X,
 // else v = w / wn, and stop once the estimate moves by at most 1e-4 relative
 // (after round 0).  One CTA.
 static __global__ void k_pw_step(int p, const double* w, double* v, double* ps) {
+  constexpr int CH = 2048;  // v, w staged through shared memory in chunks
+  __shared__ double cv[CH], cw[CH];
   __shared__ int s_dec;
   __shared__ double s_wn;
   if (ps[0] != 0.0) return;
+  double next = 0.0, nrm2 = 0.0;  // thread 0's sequential sums (the oracle's order)
+  for (int c0 = 0; c0 < p; c0 += CH) {
+    const int len = min(CH, p - c0);
+    for (int j = threadIdx.x; j < len; j += blockDim.x) {
+      cv[j] = v[c0 + j];
+      cw[j] = w[c0 + j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int j = 0; j < len; ++j) next = __dadd_rn(next, __dmul_rn(cv[j], cw[j]));
+    __syncthreads();
+  }
+  for (int c0 = 0; c0 < p; c0 += CH) {
+    const int len = min(CH, p - c0);
+    for (int j = threadIdx.x; j < len; j += blockDim.x) cw[j] = w[c0 + j];
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int j = 0; j < len; ++j) nrm2 = __dadd_rn(nrm2, __dmul_rn(cw[j], cw[j]));
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
-    double next = 0.0, nrm2 = 0.0;
-    for (int j = 0; j < p; ++j) next = __dadd_rn(next, __dmul_rn(v[j], w[j]));
-    for (int j = 0; j < p; ++j) nrm2 = __dadd_rn(nrm2, __dmul_rn(w[j], w[j]));
     const double wn = sqrt(nrm2);
     int dec = 0;  // 0: continue, 1: zero / non-positive, 2: converged
     if (wn == 0.0 || next <= 0.0)
