@@ -792,26 +792,34 @@ static __global__ void __launch_bounds__(256) k_pw_xv(int n, int p, const double
 }
 
 // w = X' xv, one warp per column: the lanes load 32 consecutive rows of the
-// column (coalesced) and form the products; lane 0 adds them in row order.
+// column (coalesced) and form the products, staged in shared memory; lane 0
+// adds them in row order (the chain of n dependent adds is the floor).
 static __global__ void __launch_bounds__(256) k_pw_xtv(int n, int p, const double* __restrict__ X,
                                                        const double* __restrict__ xv,
                                                        double* __restrict__ w, const double* ps) {
+  __shared__ double prods[8][2][32];
   if (ps[0] != 0.0) return;
-  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+  const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + wp;
   if (j >= p) return;
   const double* col = X + (size_t)j * n;
   double s = 0.0;
-  double prod = lane < n ? __dmul_rn(col[lane], xv[lane]) : 0.0;
-  for (int i0 = 0; i0 < n; i0 += 32) {
-    const int in = i0 + 32 + lane;  // next chunk's product, ahead of the chain
+  int buf = 0;
+  prods[wp][0][lane] = lane < n ? __dmul_rn(col[lane], xv[lane]) : 0.0;
+  for (int i0 = 0; i0 < n; i0 += 32, buf ^= 1) {
+    const int in = i0 + 32 + lane;  // next chunk's products, ahead of the chain
     const double nprod = in < n ? __dmul_rn(col[in], xv[in]) : 0.0;
-    const int cnt = min(32, n - i0);
-    for (int q = 0; q < cnt; ++q) {
-      const double t = __shfl_sync(0xffffffffu, prod, q);
-      s = __dadd_rn(s, t);  // lane 0's chain is the one kept
+    __syncwarp();
+    if (lane == 0) {
+      const double* pr = prods[wp][buf];
+      if (i0 + 32 <= n) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) s = __dadd_rn(s, pr[q]);
+      } else {
+        for (int q = 0; q < n - i0; ++q) s = __dadd_rn(s, pr[q]);
+      }
     }
-    prod = nprod;
+    prods[wp][buf ^ 1][lane] = nprod;
   }
   if (lane == 0) w[j] = s;
 }
