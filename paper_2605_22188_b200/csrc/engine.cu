@@ -282,6 +282,10 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
   {  // active width from which the 128 x 64 GEMM tiles are used (BNBG_BIGGEMM=0: never)
     const char* e = getenv("BNBG_BIGGEMM");
     big_min_ = e ? std::max(0, atoi(e)) : 64;
+    // ... and from which the standalone iteration GEMMs run on the tcgen05
+    // emulation (measured at c4: 16 beats 32 and 64 by 3-4 %)
+    const char* o = getenv("BNBG_OZAKI_MIN");
+    oz_min_ = o ? std::max(1, atoi(o)) : 16;
   }
   // batch workspaces and the node pool sized for a typical narrow frontier up
   // front, so the first passes of a solve do not pay cudaMalloc/cudaFree
@@ -562,7 +566,7 @@ int Engine::compute_smoothness(double* out) {
 int Engine::step(int ma, double eta, double rho, const RelaxParams& cfg) {
   const GemmPlan p1 = plan(n, p, ma, false);
   tic(KC_GEMM_NN);
-  if (p1.big && ozaki_enabled()) {  // tcgen05 kind::i8 emulated FP64 + l' epilogue
+  if (ma >= oz_min_ && ozaki_enabled()) {  // tcgen05 kind::i8 emulated FP64 + l' epilogue
     if (int rc = gemm_ozaki(false, true, dV_, p, dAct_, ma, dMa_, dR_, n, 0, nullptr)) return rc;
   } else if (int rc = launch_gemm(false, EPI_DERIV, p1, dV_, p, dR_, n, dAct_, dMa_, 0, mcap_)) {
     return rc;
@@ -571,7 +575,7 @@ int Engine::step(int ma, double eta, double rho, const RelaxParams& cfg) {
   const GemmPlan p2 = plan(p, n, ma, true);
   tic(KC_GEMM_TN);
   int tn_split = p2.nsplit;
-  if (p2.big && ozaki_enabled()) {  // tcgen05 kind::i8 emulated FP64 (ozaki.cuh)
+  if (ma >= oz_min_ && ozaki_enabled()) {  // tcgen05 kind::i8 emulated FP64 (ozaki.cuh)
     if (int rc = gemm_ozaki(true, false, dR_, n, dAct_, ma, dMa_, dG_, p, (long long)p * mcap_, &tn_split))
       return rc;
   } else if (int rc = launch_gemm(true, EPI_STORE, p2, dR_, n, dG_, p, dAct_, dMa_,
@@ -1124,7 +1128,7 @@ int Engine::gemm_probe(int trans, int m, const double* Bh, double* Ch) {
   if (int rc_ = h2d(dMa_, &m, sizeof(int))) return rc_;
   const GemmPlan pl = plan(Mo, K, m, trans != 0);
   int ns = pl.nsplit;
-  if (pl.big && ozaki_enabled()) {
+  if (m >= oz_min_ && ozaki_enabled()) {
     if (int rc = gemm_ozaki(trans != 0, false, dBin, K, nullptr, m, dMa_, dC, Mo,
                             (long long)Mo * m, &ns))
       return rc;

@@ -234,6 +234,7 @@ class Engine {
   int* hPin_ = nullptr;   // pinned: [0] ma, [1] err
   int nsplit_max_ = 8;
   int big_min_ = 64;  // m_a from which the 128 x 64 register-tiled GEMM is used
+  int oz_min_ = 16;   // m_a from which the standalone iteration GEMMs use the tcgen05 emulation
   double persist_max_flops_ = 4e9;  // streaming mode: persistent kernel up to this work per iteration
   int nrb_max_ = 1;
   int cur_nsplit_ = 1;

@@ -88,8 +88,8 @@ int Engine::gemm_ozaki(bool tn, bool deriv, const double* Bsrc, int ldb, const i
   // split: the l' epilogue needs whole sums): the tile width with the fewer
   // wave-weighted tile costs.
   const int mt = (M + kOzBM - 1) / kOzBM;
-  int bn = 64;
-  if (!tn) {  // waves x per-tile cost (a 32-column tile costs ~0.6 of a 64-column one:
+  int bn = ma <= 32 ? 32 : 64;
+  if (!tn && ma > 32) {  // waves x per-tile cost (a 32-column tile costs ~0.6 of a 64-column one:
               // the A digits it loads are the same)
     const int t64 = mt * ((ma + 63) / 64), t32 = mt * ((ma + 31) / 32);
     const double c64 = (double)((t64 + sms_ - 1) / sms_), c32 = 0.6 * ((t32 + sms_ - 1) / sms_);

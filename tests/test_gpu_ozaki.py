@@ -18,7 +18,7 @@ def test_ozaki_tn_matches_fp64(bnb, n, p):
     rng = np.random.default_rng(n)
     cases = []
     for trans in (True, False):
-        for m in (64, 100, 300):
+        for m in (20, 33, 64, 100, 300):
             B = rng.normal(size=(n if trans else p, m)) * rng.choice([1e-3, 1.0, 50.0])
             if m == 100:
                 B[:, 7] = 0.0  # an all-zero column (exponent 0, all digits 0)
