@@ -537,21 +537,35 @@ int Engine::compute_smoothness(double* out) {
   // the host synchronises once per batch instead of once per round; the
   // arithmetic is the oracle's sequential order (bit-identical L)
   double ps[4] = {0.0, 0.0, -1.0, 0.0};
-  for (int launched = 0; launched < 100;) {
-    const int batch = std::min(launched == 0 ? 4 : 8, 100 - launched);
-    for (int b = 0; b < batch; ++b) {
-      k_pw_xv<<<(n + 255) / 256, 256, 0, stream_>>>(n, p, dX_, dv, dxv, dps);
-      CKL("k_pw_xv");
-      k_pw_xtv<<<(p + 7) / 8, 256, 0, stream_>>>(n, p, dX_, dxv, dw, dps);  // a warp per column
-      CKL("k_pw_xtv");
-      k_pw_step<<<1, 256, 0, stream_>>>(p, dw, dv, dps);
-      CKL("k_pw_step");
-    }
-    launched += batch;
-    if (int rc_ = d2h(ps, dps, sizeof(ps))) return rc_;
-    CK(cudaStreamSynchronize(stream_));
-    if (ps[0] != 0.0) break;
+  // 8 rounds (24 kernels) captured once as a CUDA graph and replayed: the
+  // kernels of rounds past the stop or past round 100 return at once
+  constexpr int kRounds = 8;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  CK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+  for (int b = 0; b < kRounds; ++b) {
+    k_pw_xv<<<(n + 255) / 256, 256, 0, stream_>>>(n, p, dX_, dv, dxv, dps);
+    k_pw_xtv<<<(p + 7) / 8, 256, 0, stream_>>>(n, p, dX_, dxv, dw, dps);  // a warp per column
+    k_pw_step<<<1, 256, 0, stream_>>>(p, dw, dv, dps);
   }
+  const cudaError_t ce = cudaStreamEndCapture(stream_, &graph);
+  if (ce != cudaSuccess) return cuda_fail(ce, "power iteration: graph capture");
+  cudaError_t ge = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ge != cudaSuccess) return cuda_fail(ge, "power iteration: graph instantiate");
+  for (int launched = 0; launched < 100; launched += kRounds) {
+    launches += 3 * kRounds;
+    ge = cudaGraphLaunch(exec, stream_);
+    if (ge != cudaSuccess) break;
+    if (int rc_ = d2h(ps, dps, sizeof(ps))) {
+      cudaGraphExecDestroy(exec);
+      return rc_;
+    }
+    ge = cudaStreamSynchronize(stream_);
+    if (ge != cudaSuccess || ps[0] != 0.0) break;
+  }
+  cudaGraphExecDestroy(exec);
+  if (ge != cudaSuccess) return cuda_fail(ge, "power iteration");
   const double estimate = ps[1];
   double result = ps[2];
   if (result < 0.0) result = std::max(1.01 * c * estimate, 1e-12);

@@ -760,7 +760,7 @@ static __global__ void __launch_bounds__(kReoptFastThreads)
 static __global__ void __launch_bounds__(256) k_pw_xv(int n, int p, const double* __restrict__ X,
                                                       const double* __restrict__ v,
                                                       double* __restrict__ xv, const double* ps) {
-  if (ps[0] != 0.0) return;
+  if (ps[0] != 0.0 || ps[3] >= 100.0) return;  // stopped, or past losses.hpp:98's 100 rounds
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   constexpr int U = 16;
@@ -798,7 +798,7 @@ static __global__ void __launch_bounds__(256) k_pw_xtv(int n, int p, const doubl
                                                        const double* __restrict__ xv,
                                                        double* __restrict__ w, const double* ps) {
   __shared__ double prods[8][2][32];
-  if (ps[0] != 0.0) return;
+  if (ps[0] != 0.0 || ps[3] >= 100.0) return;  // stopped, or past losses.hpp:98's 100 rounds
   const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x * (blockDim.x >> 5) + wp;
   if (j >= p) return;
@@ -833,7 +833,7 @@ static __global__ void k_pw_step(int p, const double* w, double* v, double* ps) 
   __shared__ double cv[CH], cw[CH];
   __shared__ int s_dec;
   __shared__ double s_wn;
-  if (ps[0] != 0.0) return;
+  if (ps[0] != 0.0 || ps[3] >= 100.0) return;  // stopped, or past losses.hpp:98's 100 rounds
   double next = 0.0, nrm2 = 0.0;  // thread 0's sequential sums (the oracle's order)
   for (int c0 = 0; c0 < p; c0 += CH) {
     const int len = min(CH, p - c0);
