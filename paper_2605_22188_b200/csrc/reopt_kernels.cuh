@@ -513,7 +513,10 @@ __global__ void __launch_bounds__(kReoptClusterThreads)
 // shared memory, column-major so consecutive threads read consecutive rows
 // (conflict-free), with up to 16 CTAs per support (non-portable cluster
 // size); the exchange is k_reopt_cluster_mb's st.async + mbarrier scheme.
-constexpr int kReoptSmemThreads = 256;
+#ifndef BNBG_REOPT_SMEM_THREADS
+#define BNBG_REOPT_SMEM_THREADS 256
+#endif
+constexpr int kReoptSmemThreads = BNBG_REOPT_SMEM_THREADS;
 constexpr int kReoptSmemMaxCluster = 16;
 
 template <int QMAX>
