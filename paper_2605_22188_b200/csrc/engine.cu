@@ -46,6 +46,32 @@ static void pinned_slot_release(int* s) {
   g_pin_free.push_back(s);
 }
 
+// pinned readback staging buffers, pooled like the slots above
+constexpr size_t kStageBytes = 4u << 20;
+static std::vector<char*> g_stage_free;
+
+static char* stage_acquire() {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (!g_stage_free.empty()) {
+      char* s = g_stage_free.back();
+      g_stage_free.pop_back();
+      return s;
+    }
+  }
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, kStageBytes, cudaHostAllocPortable) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;  // readbacks then stay pageable
+  }
+  return static_cast<char*>(p);
+}
+
+static void stage_release(char* s) {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_stage_free.push_back(s);
+}
+
 #define CK(call)                                          \
   do {                                                    \
     cudaError_t e_ = (call);                              \
@@ -118,6 +144,7 @@ Engine::~Engine() {
   // stream before the slot returns to the process-wide free list
   if (stream_) cudaStreamSynchronize(stream_);
   if (hPin_) pinned_slot_release(hPin_);
+  if (hStage_) stage_release(hStage_);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -168,11 +195,13 @@ int Engine::make_tmaps() {
 
 int Engine::fail(int code, const std::string& msg) {
   err = msg;
+  defer_.clear();  // queued readbacks of the failed call are never copied out
   return code;
 }
 
 int Engine::cuda_fail(cudaError_t e, const char* what) {
   err = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+  defer_.clear();
   return 4;  // BNBG_CUDA_ERROR
 }
 
@@ -211,6 +240,11 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
   CK(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device));
   hPin_ = pinned_slot_acquire();
   if (!hPin_) return cuda_fail(cudaErrorMemoryAllocation, "cudaMallocHost");
+  {
+    const char* de = getenv("BNBG_DEFER_D2H");
+    defer_on_ = !(de && de[0] == '0');
+    if (defer_on_) hStage_ = stage_acquire();
+  }
   stamp("malloc_host");
   CK(cudaMallocAsync(&dX_, sizeof(double) * (size_t)n * p, stream_));
   CK(cudaMallocAsync(&dy_, sizeof(double) * (size_t)n, stream_));
@@ -259,9 +293,29 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
           pass_smem_ = rb;
         }
       }
+      // one-cluster variant for small X (c1): 16 CTAs of one cluster hold X
+      // (64-row NN tiles) and meet at cluster barriers, 0.2 us against the
+      // grid barrier's 1.2 us (profiles/r02_barriers.txt); narrow batches only,
+      // as it has 16 SMs (BNBG_CLUSTER_PASS=0 disables it, BNBG_CLUSTER_MAXM
+      // sets the widest batch)
+      resc_ = ResLayout{};
+      const char* cenv = getenv("BNBG_CLUSTER_PASS");
+      if (res_.on && !(cenv && cenv[0] == '0')) {
+        constexpr int kCS = 16;
+        ResLayout Lc;
+        const size_t rbc = pass_res_plan(n, p, n2_, colE_, kCS, limit, &Lc, 4);
+        if (Lc.on && Lc.off_cc > 0 && pass_cluster_ok(colE_, rbc, kCS)) {
+          Lc.cluster = kCS;
+          resc_ = Lc;
+          pass_smem_c_ = rbc;
+        }
+        (void)cudaGetLastError();
+        const char* me = getenv("BNBG_CLUSTER_MAXM");
+        if (me) cluster_max_m_ = atoi(me);
+      }
       if (pass_smem_ <= limit) {
         int nb = 0;
-        CK(pass_setup(colE_, pass_smem_, &nb));
+        CK(pass_setup(colE_, std::max(pass_smem_, pass_smem_c_), &nb));
         if (nb >= 1) pass_grid_ = sms_;
       }
     }
@@ -421,6 +475,32 @@ int Engine::d2h(void* dst, const void* src, size_t bytes) {
   if (!bytes) return 0;
   d2h_bytes += (long long)bytes;
   CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream_));
+  return 0;
+}
+int Engine::d2h_defer(void* dst, const void* src, size_t bytes) {
+  if (!bytes) return 0;
+  if (!hStage_ || bytes > kStageBytes) return d2h(dst, src, bytes);
+  size_t off = (stage_used_ + 15) & ~(size_t)15;
+  if (off + bytes > kStageBytes) {
+    if (int rc = sync_flush()) return rc;
+    off = 0;
+  }
+  d2h_bytes += (long long)bytes;
+  CK(cudaMemcpyAsync(hStage_ + off, src, bytes, cudaMemcpyDeviceToHost, stream_));
+  defer_.push_back(Deferred{dst, off, bytes});
+  stage_used_ = off + bytes;
+  return 0;
+}
+
+int Engine::sync_flush() {
+  const cudaError_t e = cudaStreamSynchronize(stream_);
+  if (e != cudaSuccess) {
+    defer_.clear();  // the destinations are not written on a failed stream
+    return cuda_fail(e, "cudaStreamSynchronize");
+  }
+  for (const Deferred& d : defer_) std::memcpy(d.dst, hStage_ + d.off, d.bytes);
+  defer_.clear();
+  stage_used_ = 0;
   return 0;
 }
 
@@ -704,7 +784,6 @@ int Engine::evaluate(int ma, double eta, double rho, const RelaxParams& cfg, int
 // (pass_kernel.cuh).  Same per-phase code as the multi-kernel path.
 int Engine::run_pass(int m, const RelaxParams& cfg, double thr, double eta, double rho,
                      double* dTrace, int& iter, int& n_evals, long long& node_its) {
-  (void)m;
   PassArgs a{};
   RelaxDev& r = a.r;
   r.p = p;
@@ -774,21 +853,25 @@ int Engine::run_pass(int m, const RelaxParams& cfg, double thr, double eta, doub
   a.nn.probe = dPassProf_ ? dPassProf_ + 20 : nullptr;
   a.tn.probe = dPassProf_ ? dPassProf_ + 24 : nullptr;
   a.bar = dBar_;
-  a.res = res_;
+  const bool clus = resc_.on && m <= cluster_max_m_;
+  a.res = clus ? resc_ : res_;
   a.big = ((n % 2) == 0 && (p % 2) == 0) ? big_min_ : 0;
   a.nn.tmap = res_.on ? nullptr : tmNN_;  // streaming mode's 128 x 64 tiles
   a.tn.tmap = res_.on ? nullptr : tmTN_;
-  CK(cudaMemsetAsync(dBar_, 0, sizeof(unsigned), stream_));
+  if (!clus) CK(cudaMemsetAsync(dBar_, 0, sizeof(unsigned), stream_));
   tic(KC_PASS);
   cudaError_t e = cudaSuccess;
-  e = pass_launch(colE_, pass_grid_, pass_smem_, stream_, &a);
+  if (clus)
+    e = pass_launch(colE_, resc_.cluster, pass_smem_c_, stream_, &a, resc_.cluster);
+  else
+    e = pass_launch(colE_, pass_grid_, pass_smem_, stream_, &a);
   ++launches;
   CK(e);
   toc(KC_PASS, 0.0);  // end event right behind the kernel, before the readback sync
   long long h_out[4] = {0, 0, 0, 0};
-  if (int rc = d2h(h_out, dPassOut_, 3 * sizeof(long long))) return rc;
+  if (int rc = d2h_defer(h_out, dPassOut_, 3 * sizeof(long long))) return rc;
   if (int rc = d2h(hPin_ + 1, dErr_, sizeof(int))) return rc;
-  CK(cudaStreamSynchronize(stream_));
+  if (int rc = sync_flush()) return rc;
   iter = (int)h_out[0];
   n_evals = (int)h_out[1];
   node_its = h_out[2];
@@ -860,25 +943,27 @@ int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_
     out.sup.resize((size_t)m * std::max(k, 1));
     out.len.resize(m);
     out.jbranch.resize(m);
-    if (int rc_ = d2h(out.sup.data(), dSup_, sizeof(int) * out.sup.size())) return rc_;
-    if (int rc_ = d2h(out.len.data(), dLen_, sizeof(int) * m)) return rc_;
-    if (int rc_ = d2h(out.jbranch.data(), dJb_, sizeof(int) * m)) return rc_;
+    if (int rc_ = d2h_defer(out.sup.data(), dSup_, sizeof(int) * out.sup.size())) return rc_;
+    if (int rc_ = d2h_defer(out.len.data(), dLen_, sizeof(int) * m)) return rc_;
+    if (int rc_ = d2h_defer(out.jbranch.data(), dJb_, sizeof(int) * m)) return rc_;
   }
   if (read_beta) {
-    if (int rc_ = d2h(out.beta.data(), dB_, sizeof(double) * (size_t)p * m)) return rc_;
+    if (int rc_ = d2h_defer(out.beta.data(), dB_, sizeof(double) * (size_t)p * m)) return rc_;
   } else {
     out.beta.clear();
   }
-  if (int rc_ = d2h(out.bounds.data(), dBest_, sizeof(double) * m)) return rc_;
-  if (int rc_ = d2h(out.status.data(), dStatus_, sizeof(int) * m)) return rc_;
-  if (int rc_ = d2h(out.iters.data(), dIters_, sizeof(int) * m)) return rc_;
+  if (int rc_ = d2h_defer(out.bounds.data(), dBest_, sizeof(double) * m)) return rc_;
+  if (int rc_ = d2h_defer(out.status.data(), dStatus_, sizeof(int) * m)) return rc_;
+  if (int rc_ = d2h_defer(out.iters.data(), dIters_, sizeof(int) * m)) return rc_;
   out.n_evals = n_evals;
   if (want_trace) {
     out.trace.resize((size_t)n_evals * m);
     for (int e = 0; e < n_evals; ++e)
-      if (int rc_ = d2h(out.trace.data() + (size_t)e * m, dTrace + (size_t)e * mcap_, sizeof(double) * m)) return rc_;
+      if (int rc_ = d2h_defer(out.trace.data() + (size_t)e * m, dTrace + (size_t)e * mcap_,
+                              sizeof(double) * m))
+        return rc_;
   }
-  CK(cudaStreamSynchronize(stream_));
+  if (int rc_ = sync_flush()) return rc_;
   resolve_timing();
 done:
   if (dTrace) dfree(dTrace);
@@ -1103,10 +1188,10 @@ int Engine::reoptimize(int nsup, const int* offsets, const int* idx, double* coe
   }
   toc(KC_REOPT, 0.0);
   std::vector<int> its(nsup);
-  if (tot) if (int rc_ = d2h(coef, d_coef, sizeof(double) * tot)) return rc_;
-  if (int rc_ = d2h(obj, d_obj, sizeof(double) * nsup)) return rc_;
-  if (int rc_ = d2h(its.data(), d_its, sizeof(int) * nsup)) return rc_;
-  CK(cudaStreamSynchronize(stream_));
+  if (tot) if (int rc_ = d2h_defer(coef, d_coef, sizeof(double) * tot)) return rc_;
+  if (int rc_ = d2h_defer(obj, d_obj, sizeof(double) * nsup)) return rc_;
+  if (int rc_ = d2h_defer(its.data(), d_its, sizeof(int) * nsup)) return rc_;
+  if (int rc_ = sync_flush()) return rc_;
   // algorithmic work of the reference iteration: 4 q n flops per support-iteration
   double flops = 0.0;
   for (int s = 0; s < nsup; ++s) {

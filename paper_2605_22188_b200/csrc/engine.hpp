@@ -182,6 +182,9 @@ class Engine {
     int nkb = 0, bcap = 0;    // K blocks (64 B), batch capacity (multiple of 64)
   } oz_[2];
   ResLayout res_{};           // X residency plan (res_.on = 0: streaming)
+  ResLayout resc_{};          // one-cluster plan for narrow batches (resc_.on = 0: none)
+  size_t pass_smem_c_ = 0;    // its dynamic shared memory
+  int cluster_max_m_ = 16;    // widest batch run by the one-cluster pass kernel
  public:
   unsigned long long* dPassProf_ = nullptr;  // phase wall times (BNBG_PASS_PROF=1)
   int pass_profile(double* ns, int count);
@@ -202,6 +205,20 @@ class Engine {
   void resolve_timing();
   int h2d(void* dst, const void* src, size_t bytes);
   int d2h(void* dst, const void* src, size_t bytes);
+  // Readbacks into pageable host memory go through a pinned staging buffer:
+  // d2h_defer queues an asynchronous copy into it, sync_flush synchronises the
+  // stream once and copies every queued block out.  (A pageable
+  // cudaMemcpyAsync blocks the host per call: ~10 us each, several per pass.)
+  int d2h_defer(void* dst, const void* src, size_t bytes);
+  int sync_flush();
+  struct Deferred {
+    void* dst;
+    size_t off, bytes;
+  };
+  std::vector<Deferred> defer_;
+  char* hStage_ = nullptr;  // pinned, kStageBytes, from the process-wide pool
+  size_t stage_used_ = 0;
+  bool defer_on_ = true;
   struct EvPair {
     cudaEvent_t a, b;
     int kc;

@@ -11,14 +11,18 @@
 namespace bnbg {
 
 // Shared-memory residency plan of X for the persistent pass kernel: CTA b
-// keeps NN row tile b (rows [16b, 16b+16) x all p, k-major, stride lda_nn)
-// and TN tile b (X columns [16 (b % tn_mt), +16) x rows of split b / tn_mt,
-// row-major, stride ldk_tn) for the whole pass; only V / R move per iteration.
+// keeps NN row tile b (rows [16 rt b, 16 rt (b+1)) x all p, k-major, stride
+// lda_nn) and TN tile b (X columns [16 (b % tn_mt), +16) x rows of split
+// b / tn_mt, row-major, stride ldk_tn) for the whole pass; only V / R move per
+// iteration.  cluster > 0: the grid is ONE thread-block cluster of that many
+// CTAs (small X, rt = 4), synchronised by cluster barriers.
 struct ResLayout {
   int on;        // 0: stream X tiles from L2/HBM (gemm_tile)
-  int nn_tiles;  // ceil(n / 16)
+  int nn_tiles;  // ceil(n / (16 rt))
   int kpad_nn;   // p rounded up to 4
-  int lda_nn;    // 20 (conflict-free DMMA fragment loads)
+  int lda_nn;    // 16 rt + 4 (conflict-free DMMA fragment loads)
+  int rt;        // 16-row sub-tiles per NN tile (1 or 4)
+  int cluster;   // 0: grid barriers over one CTA per SM; else the cluster size
   int tn_mt;     // ceil(p / 16)
   int tn_split;  // K splits of the n rows
   int tn_klen;   // rows per split (multiple of 4)
@@ -93,9 +97,12 @@ cudaError_t launch_reopt_smem(int qmax, int cs, int nsup, cudaStream_t st, int n
 size_t pass_smem(int p, int n2, int E);
 // residency plan for `grid` CTAs (res.on = 0 when X does not fit); returns the
 // dynamic shared memory the resident kernel needs
-size_t pass_res_plan(int n, int p, int n2, int E, int grid, size_t smem_limit, ResLayout* res);
+size_t pass_res_plan(int n, int p, int n2, int E, int grid, size_t smem_limit, ResLayout* res,
+                     int rt = 1);
+// true when k_pass<E> launches as one cluster of `cs` CTAs with `smem` bytes
+bool pass_cluster_ok(int E, size_t smem, int cs);
 cudaError_t pass_setup(int E, size_t smem, int* blocks_per_sm);
 cudaError_t pass_static_smem(int E, size_t* bytes);
-cudaError_t pass_launch(int E, int grid, size_t smem, cudaStream_t st, PassArgs* a);
+cudaError_t pass_launch(int E, int grid, size_t smem, cudaStream_t st, PassArgs* a, int cluster = 0);
 
 }  // namespace bnbg

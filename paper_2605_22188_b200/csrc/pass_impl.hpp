@@ -12,6 +12,8 @@ cudaError_t pass_static_smem_t(size_t* bytes);
 template <int E>
 cudaError_t pass_setup_t(size_t smem, int* blocks_per_sm);
 template <int E>
-cudaError_t pass_launch_t(int grid, size_t smem, cudaStream_t st, PassArgs* a);
+cudaError_t pass_launch_t(int grid, size_t smem, cudaStream_t st, PassArgs* a, int cluster);
+template <int E>
+bool pass_cluster_ok_t(size_t smem, int cs);
 
 }  // namespace bnbg

@@ -46,7 +46,12 @@ constexpr int kPassNW = kPassThreads / 32;
 
 __device__ __forceinline__ int pass_fn(int ma) { return ma <= 8 ? 1 : (ma <= 16 ? 2 : 4); }
 
-__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target) {
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target, int cluster) {
+  if (cluster) {  // one-cluster grid: the hardware cluster barrier (0.2 us vs 1.2 us)
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    return;
+  }
   target += gridDim.x;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -179,10 +184,10 @@ __host__ __device__ inline int ld_mod16_4(int v) {  // smallest >= v with (x % 1
 }
 
 // work region: staged B chunk (up to 16 columns x ldb), reused afterwards for
-// the cross-warp reduction (NW x 2 x FN x 64) and the l / l* staging (2 x 16 x 16)
+// the cross-warp reduction (NW x 2 x FN x 64) and the l / l* staging (2 x 16 rt x 16)
 __host__ __device__ inline size_t res_work_doubles(const ResLayout& r) {
   size_t b = (size_t)16 * r.ldb;
-  const size_t red = (size_t)kPassNW * 2 * 2 * 64 + 2 * 16 * 16;
+  const size_t red = (size_t)kPassNW * 2 * 2 * 64 + 2 * 16 * r.rt * 16;
   return b > red ? b : red;
 }
 
@@ -192,10 +197,11 @@ static __device__ void res_load_x(const PassArgs& a, double* smem) {
   const double* X = a.nn.A;
   const int n = a.n, p = a.p;
   if ((int)blockIdx.x < L.nn_tiles) {
-    const int m0 = blockIdx.x * kResBM;
+    const int bm = kResBM * L.rt;
+    const int m0 = blockIdx.x * bm;
     double* A = smem;
-    for (int e = threadIdx.x; e < L.kpad_nn * kResBM; e += kPassThreads) {
-      const int k = e / kResBM, m = e % kResBM;
+    for (int e = threadIdx.x; e < L.kpad_nn * bm; e += kPassThreads) {
+      const int k = e / bm, m = e % bm;
       A[k * L.lda_nn + m] = (k < p && m0 + m < n) ? X[(size_t)k * n + m0 + m] : 0.0;
     }
   }
@@ -212,15 +218,19 @@ static __device__ void res_load_x(const PassArgs& a, double* smem) {
   __syncthreads();
 }
 
-// One output tile (16 rows x 8*FN compact columns starting at n0) from the
+// One output tile (16 RT rows x 8*FN compact columns starting at n0) from the
 // resident A operand: NN  A[k*lda + m] (K = kpad_nn), TN  A[m*lda + k] (K = tn_klen).
 // B chunk: column c at g.B + col*g.ldb + kbeg, kvalid valid rows (rest zero).
-template <bool TN, int FN, int EPI>
+// RT 16-row sub-tiles share the staged B chunk; warp w computes sub-tile
+// w % RT over the k-steps w / RT (mod NW / RT).
+template <bool TN, int FN, int EPI, int RT = 1>
 __device__ void res_tile(const GemmArgs& g, const double* Ares, int lda, int K, int kbeg,
                          int kvalid, int m0, int mt, int n0, int ncols, int split, double* work,
                          int ldb, int* colmap) {
-  constexpr int FM = 2, BM = 16, BN = 8 * FN, NW = kPassNW, NT = kPassThreads;
+  constexpr int FM = 2, BM = 16 * RT, BN = 8 * FN, NW = kPassNW, NT = kPassThreads, KW = NW / RT;
+  static_assert(!TN || RT == 1, "TN tiles are 16 columns of X");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sub = warp % RT, kw = warp / RT;
   ColProbe pr(g.probe);
   if (tid < BN) {
     const int c = n0 + tid;
@@ -272,7 +282,7 @@ __device__ void res_tile(const GemmArgs& g, const double* Ares, int lda, int K, 
     double av[FM], bv[FN];
 #pragma unroll
     for (int i = 0; i < FM; ++i) {
-      const int row = i * 8 + (lane >> 2);
+      const int row = sub * 16 + i * 8 + (lane >> 2);
       av[i] = TN ? Ares[row * lda + kk] : Ares[kk * lda + row];
     }
 #pragma unroll
@@ -282,10 +292,10 @@ __device__ void res_tile(const GemmArgs& g, const double* Ares, int lda, int K, 
 #pragma unroll
       for (int j = 0; j < FN; ++j) dmma_8x8x4(acc[u][i][j][0], acc[u][i][j][1], av[i], bv[j]);
   };
-  int ks = warp;
-  for (; ks + NW < nks; ks += 2 * NW) {
+  int ks = kw;
+  for (; ks + KW < nks; ks += 2 * KW) {
     kstep(0, ks);
-    kstep(1, ks + NW);
+    kstep(1, ks + KW);
   }
   if (ks < nks) kstep(0, ks);
 #pragma unroll
@@ -310,13 +320,14 @@ __device__ void res_tile(const GemmArgs& g, const double* Ares, int lda, int K, 
   double* Cout = g.C + (size_t)split * g.split_stride;
   for (int e = tid; e < BM * BN; e += NT) {
     const int c = e / BM, r = e % BM;
-    const int i = r >> 3, j = c >> 3;
-    const int ln = (r & 7) * 4 + ((c & 7) >> 1), h = c & 1;
-    const int off = (i * FN + j) * 64 + h * 32 + ln;
+    const int rs = r >> 4, rr = r & 15;
+    const int i = rr >> 3, j = c >> 3;
+    const int ln = (rr & 7) * 4 + ((c & 7) >> 1), h = c & 1;
     constexpr int stride_w = FM * FN * 64;
+    const int off = (i * FN + j) * 64 + h * 32 + ln + rs * stride_w;
     double s = red[off];
 #pragma unroll
-    for (int w = 1; w < NW; ++w) s += red[off + w * stride_w];
+    for (int w = 1; w < KW; ++w) s += red[off + w * RT * stride_w];
     const int gm = m0 + r;
     const int col = colmap[c];
     if (EPI == EPI_STORE) {
@@ -363,14 +374,22 @@ __device__ void res_phase_nn(const PassArgs& a, const double* Bsrc, int ma, doub
   g.B = Bsrc;
   g.act = act;
   double* work = smem + L.off_work;
-  const int m0 = blockIdx.x * kResBM;
+  const int m0 = blockIdx.x * kResBM * L.rt;
   for (int n0 = 0; n0 < ma; n0 += 16) {
-    if (ma - n0 > 8)
+    if (L.rt == 4) {
+      if (ma - n0 > 8)
+        res_tile<false, 2, EPI, 4>(g, smem, L.lda_nn, L.kpad_nn, 0, a.p, m0, blockIdx.x, n0, ma,
+                                   0, work, L.ldb, colmap);
+      else
+        res_tile<false, 1, EPI, 4>(g, smem, L.lda_nn, L.kpad_nn, 0, a.p, m0, blockIdx.x, n0, ma,
+                                   0, work, L.ldb, colmap);
+    } else if (ma - n0 > 8) {
       res_tile<false, 2, EPI>(g, smem, L.lda_nn, L.kpad_nn, 0, a.p, m0, blockIdx.x, n0, ma, 0,
                               work, L.ldb, colmap);
-    else
+    } else {
       res_tile<false, 1, EPI>(g, smem, L.lda_nn, L.kpad_nn, 0, a.p, m0, blockIdx.x, n0, ma, 0,
                               work, L.ldb, colmap);
+    }
   }
 }
 
@@ -488,16 +507,16 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
   auto evaluate = [&](int it) {  // relaxation.hpp:194-221
     phase_nn(r.B, true);
     arrive(PH_EVNN);
-    grid_barrier(a.bar, bar_target);
+    grid_barrier(a.bar, bar_target, a.res.cluster);
     mark(PH_EVNN);
     nsplit = phase_tn();
     arrive(PH_EVTN);
-    grid_barrier(a.bar, bar_target);
+    grid_barrier(a.bar, bar_target, a.res.cluster);
     mark(PH_EVTN);
     EvalArgs e;
     e.part_loss = a.nn.part_loss;
     e.part_conj = a.nn.part_conj;
-    e.nrb = !res && pass_big(a, ma) ? (a.n + kBigBM - 1) / kBigBM : (a.n + 15) / 16;
+    e.nrb = res ? a.res.nn_tiles : (pass_big(a, ma) ? (a.n + kBigBM - 1) / kBigBM : (a.n + 15) / 16);
     e.part_ld = a.nn.part_ld;
     e.iter = it;
     e.prune_threshold = a.prune_thr;
@@ -509,11 +528,11 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
     else
       for (int c = blockIdx.x; c < ma; c += gridDim.x) eval_column<E>(r, nsplit, e, c, colsm);
     arrive(PH_EVCOL);
-    grid_barrier(a.bar, bar_target);
+    grid_barrier(a.bar, bar_target, a.res.cluster);
     mark(PH_EVCOL);
     if (blockIdx.x == 0) compact_active<kPassThreads>(r.act, r.d_ma, r.frozen);
     arrive(PH_COMPACT);
-    grid_barrier(a.bar, bar_target);
+    grid_barrier(a.bar, bar_target, a.res.cluster);
     mark(PH_COMPACT);
     refresh();
     // non-finite iterate (numeric_error, relaxation.hpp:76-81): stop early;
@@ -526,18 +545,18 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
     ++iter;
     phase_nn(r.V, false);
     arrive(PH_NN);
-    grid_barrier(a.bar, bar_target);
+    grid_barrier(a.bar, bar_target, a.res.cluster);
     mark(PH_NN);
     nsplit = phase_tn();
     arrive(PH_TN);
-    grid_barrier(a.bar, bar_target);
+    grid_barrier(a.bar, bar_target, a.res.cluster);
     mark(PH_TN);
     if (cached)
       cc.t = prox_column_impl<E, true>(r, nsplit, blockIdx.x, colsm, cc);
     else
       for (int c = blockIdx.x; c < ma; c += gridDim.x) prox_column<E>(r, nsplit, c, colsm);
     arrive(PH_PROX);
-    grid_barrier(a.bar, bar_target);
+    grid_barrier(a.bar, bar_target, a.res.cluster);
     mark(PH_PROX);
     node_its += ma;
     if (iter % a.check == 0) {

@@ -29,11 +29,13 @@ namespace bnbg {
 
 size_t pass_smem(int p, int n2, int E) { return pass_smem_bytes(p, n2, E); }
 
-size_t pass_res_plan(int n, int p, int n2, int E, int grid, size_t smem_limit, ResLayout* res) {
+size_t pass_res_plan(int n, int p, int n2, int E, int grid, size_t smem_limit, ResLayout* res,
+                     int rt) {
   ResLayout L = {};
-  L.nn_tiles = (n + kResBM - 1) / kResBM;
+  L.rt = rt;
+  L.nn_tiles = (n + kResBM * rt - 1) / (kResBM * rt);
   L.kpad_nn = (p + 3) & ~3;
-  L.lda_nn = kResBM + 4;
+  L.lda_nn = kResBM * rt + 4;
   L.tn_mt = (p + kResBM - 1) / kResBM;
   *res = L;
   if (L.nn_tiles > grid || L.tn_mt > grid) return 0;
@@ -78,10 +80,16 @@ cudaError_t pass_setup(int E, size_t smem, int* blocks_per_sm) {
   return e;
 }
 
-cudaError_t pass_launch(int E, int grid, size_t smem, cudaStream_t st, PassArgs* a) {
+cudaError_t pass_launch(int E, int grid, size_t smem, cudaStream_t st, PassArgs* a, int cluster) {
   cudaError_t e = cudaSuccess;
-  DISPATCH_E(E, e = pass_launch_t<EV>(grid, smem, st, a));
+  DISPATCH_E(E, e = pass_launch_t<EV>(grid, smem, st, a, cluster));
   return e;
+}
+
+bool pass_cluster_ok(int E, size_t smem, int cs) {
+  bool ok = false;
+  DISPATCH_E(E, ok = pass_cluster_ok_t<EV>(smem, cs));
+  return ok;
 }
 
 }  // namespace bnbg

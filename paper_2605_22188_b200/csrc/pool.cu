@@ -139,17 +139,17 @@ int Engine::branch_pool(int m, const int* slots, const double* lb_in, double pos
                                                    dLbOut_, dFree_, dRec_, dRecLb_);
   CKL("k_branch_write");
   int tot[2];
-  if (int rc_ = d2h(tot, dTot_, sizeof(tot))) return rc_;
-  CK(cudaStreamSynchronize(stream_));
+  if (int rc_ = d2h_defer(tot, dTot_, sizeof(tot))) return rc_;
+  if (int rc_ = sync_flush()) return rc_;
   survivors = tot[0];
   bad_column = tot[1];
   const size_t nc = 2 * (size_t)survivors;
   rec.resize(nc * RI);
   rec_lb.resize(nc);
   if (nc) {
-    if (int rc_ = d2h(rec.data(), dRec_, sizeof(int) * nc * RI)) return rc_;
-    if (int rc_ = d2h(rec_lb.data(), dRecLb_, sizeof(double) * nc)) return rc_;
-    CK(cudaStreamSynchronize(stream_));
+    if (int rc_ = d2h_defer(rec.data(), dRec_, sizeof(int) * nc * RI)) return rc_;
+    if (int rc_ = d2h_defer(rec_lb.data(), dRecLb_, sizeof(double) * nc)) return rc_;
+    if (int rc_ = sync_flush()) return rc_;
   }
   (void)slots;
   return 0;

@@ -300,3 +300,39 @@ def test_errors(bnb, orc):
     warm[2, 0] = np.nan
     with pytest.raises(bnb.NumericError):
         eng.solve_batch_relaxation((np.zeros((10, 1)), [3], warm))
+
+
+@pytest.mark.parametrize("cluster", ["1", "0"])
+@pytest.mark.parametrize("loss,m", [(0, 5), (1, 16), (0, 20)])
+def test_relax_one_cluster_pass_kernel(bnb, orc, monkeypatch, cluster, loss, m):
+    """c1-sized X (n=1000, p=100) fits one 16-CTA cluster: batches of up to 16
+    columns run the pass kernel as ONE cluster (64-row resident NN tiles,
+    cluster barriers); BNBG_CLUSTER_PASS=0 forces the 148-CTA grid-barrier
+    kernel.  Both match the oracle (m = 20 takes the grid kernel either way)."""
+    monkeypatch.setenv("BNBG_CLUSTER_PASS", cluster)
+    inst, eng = _engine(bnb, orc, 1000, 100, 5, 0.5, loss, seed=11)
+    rng = np.random.default_rng(m * 7 + loss)
+    st, kb = rnd_batch(rng, 100, m, 5, all_free_first=True)
+    warm = np.zeros((100, m))
+    L = orc.smoothness(loss, inst.X)
+    res = eng.solve_batch_relaxation((st, kb, warm), bnb.RelaxConfig(smoothness=L), math.inf)
+    ob, obnd, ost, oit = orc.relax_batch(inst, st, kb, warm, math.inf, orc.relax_cfg(smoothness=L))
+    np.testing.assert_allclose(res.bounds, obnd, rtol=1e-6, atol=1e-6)
+    assert res.status.tolist() == ost.tolist()
+    assert res.iterations.tolist() == oit.tolist()
+    np.testing.assert_allclose(res.beta, ob, rtol=1e-6, atol=1e-7)
+
+
+def test_c1_certificate_same_with_and_without_cluster_pass(bnb, monkeypatch):
+    """c1 (BASELINE configs[0]) certified by the one-cluster pass kernel and by
+    the grid kernel: the reference's support, objective and node count."""
+    inst, _ = bnb.generate_synthetic(bnb.GeneratorSpec(n=1000, p=100, k=5, correlation=0.5,
+                                                       loss=bnb.LossKind.SQUARED, seed=0))
+    certs = {}
+    for cluster in ("1", "0"):
+        monkeypatch.setenv("BNBG_CLUSTER_PASS", cluster)
+        certs[cluster] = bnb.solve(inst, bnb.SolverConfig())
+    for c in certs.values():
+        assert c.status == "optimal" and c.support == [19, 39, 59, 79, 99]
+        assert c.nodes_processed == 43
+        assert abs(c.optimal_value - 6562.563358901953) <= 1e-9 * 6562.6
