@@ -655,10 +655,6 @@ int run_bnb(bnbg_handle* h, const bnbg_solver_cfg& cfg, Policy& pol, bnbg_certif
 // ===========================================================================
 // C-ABI
 // ===========================================================================
-extern "C" {
-
-}  // extern "C" (helper below is internal)
-
 // The pool pass seam is two calls (bnbg_pool_relax, then bnbg_pool_branch)
 // sharing the batch workspaces (slots, states, betas, status, best bounds,
 // branch variables).  Every other entry point that may write those buffers

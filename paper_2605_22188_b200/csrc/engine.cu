@@ -120,6 +120,10 @@ Engine::~Engine() {
   dfree(dPassProf_);
   dfree(dBar_);
   dfree(dTmap_);
+  dfree(dTmapQ_);
+  dfree(dQ_);
+  dfree(dCq_);
+  dfree(dGramCnt_);
   dfree(dColScr_);
   for (OzSide& S : oz_) {
     dfree(S.dX);
@@ -278,12 +282,17 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     pass_grid_ = 0;
     res_ = ResLayout{};
+    {
+      const char* ge = getenv("BNBG_GRAM");
+      gram_ = loss == kSquared && p <= n && !(ge && ge[0] == '0');
+    }
     if (coop && !(env && env[0] == '0')) {
       size_t stat = 0;
       CK(pass_static_smem(colE_, &stat));
       const size_t limit = (size_t)optin - stat - 256;
       pass_smem_ = pass_smem(p, n2_, colE_);
-      if (!(renv && renv[0] == '0')) {
+      // Gram iterations stream Q from L2; X is read at evaluations only
+      if (!(renv && renv[0] == '0') && !gram_) {
         ResLayout L;
         const size_t rb = pass_res_plan(n, p, n2_, colE_, sms_, limit, &L);
         if (L.on) {
@@ -508,10 +517,10 @@ int Engine::sync_flush() {
 // GEMM planning: BN from the active width, BM so the grid covers the SMs,
 // split-K (TN only) when the tiles alone cannot.
 // ---------------------------------------------------------------------------
-Engine::GemmPlan Engine::plan(int Mr, int K, int ncols, bool allow_split) const {
+Engine::GemmPlan Engine::plan(int Mr, int K, int ncols, bool allow_split, bool allow_big) const {
   GemmPlan pl;
   // wide batches: register-tiled 128 x 64 tiles, no split-K (BNBG_BIGGEMM=0 disables)
-  if (big_min_ > 0 && ncols >= big_min_ && (n % 2) == 0 && (p % 2) == 0) {
+  if (allow_big && big_min_ > 0 && ncols >= big_min_ && (n % 2) == 0 && (p % 2) == 0) {
     const int bm = gemm_big_tile_m(), bn = gemm_big_tile_n(), bk = gemm_big_tile_k();
     pl.big = true;
     pl.fm = pl.fn = 0;
@@ -583,6 +592,69 @@ int Engine::launch_gemm(bool tn, int epi, const GemmPlan& pl, const double* Bsrc
     CK(gemm_big_launch(tn, epi, pl.grid, stream_, g));
   else
     CK(gemm_launch(tn, epi, pl.fm, pl.fn, pl.grid, stream_, g));
+  return 0;
+}
+
+// Q = X'X and c = X'y for the Gram-form iteration gradient (once per engine;
+// the TN product kernels, unsplit)
+int Engine::gram_prepare() {
+  if (dQ_) return 0;
+  CK(cudaMallocAsync(&dQ_, sizeof(double) * (size_t)p * p, stream_));
+  CK(cudaMallocAsync(&dCq_, sizeof(double) * (size_t)p, stream_));
+  CK(cudaMallocAsync(&dGramCnt_, 2 * sizeof(int), stream_));
+  const int cnt[2] = {p, 1};
+  if (int rc = h2d(dGramCnt_, cnt, sizeof(cnt))) return rc;
+  if (int rc = launch_gemm(true, EPI_STORE, plan(p, n, p, false), dX_, n, dQ_, p, nullptr, dGramCnt_,
+                           0, mcap_))
+    return rc;
+  if (int rc = launch_gemm(true, EPI_STORE, plan(p, n, 1, false), dy_, n, dCq_, p, nullptr,
+                           dGramCnt_ + 1, 0, mcap_))
+    return rc;
+  if (tmNN_ && p >= 132) {  // TMA descriptor of Q in the NN orientation
+    auto enc = tmap_encoder();
+    int nn[2], tn[2];
+    gemm_big_boxes(nn, tn);
+    CUtensorMap h;
+    const cuuint64_t dims[2] = {(cuuint64_t)p, (cuuint64_t)p};
+    const cuuint64_t strides[1] = {(cuuint64_t)p * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)nn[0], (cuuint32_t)nn[1]};
+    const cuuint32_t estr[2] = {1, 1};
+    if (enc && enc(&h, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, dQ_, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+      CK(cudaMallocAsync(&dTmapQ_, sizeof(h), stream_));
+      CK(cudaMemcpyAsync(dTmapQ_, &h, sizeof(h), cudaMemcpyHostToDevice, stream_));
+      CK(cudaStreamSynchronize(stream_));
+    }
+  }
+  return 0;
+}
+
+// G[:, act] = Q V[:, act] - c (l' of the squared loss with y = c: EPI_DERIV)
+int Engine::launch_gram(const GemmPlan& pl, const double* Bsrc, int ldb, double* C, int ldc,
+                        const int* act, const int* d_ncols) {
+  GemmArgs g{};
+  g.M = p;
+  g.K = p;
+  g.A = dQ_;
+  g.lda = p;
+  g.B = Bsrc;
+  g.ldb = ldb;
+  g.C = C;
+  g.ldc = ldc;
+  g.split_stride = 0;
+  g.ksplit = pl.ksplit;
+  g.act = act;
+  g.d_ncols = d_ncols;
+  g.y = dCq_;
+  g.loss = kSquared;
+  g.part_ld = mcap_;
+  ++launches;
+  g.tmap = pl.big ? dTmapQ_ : nullptr;
+  if (pl.big)
+    CK(gemm_big_launch(false, EPI_DERIV, pl.grid, stream_, g));
+  else
+    CK(gemm_launch(false, EPI_DERIV, pl.fm, pl.fn, pl.grid, stream_, g));
   return 0;
 }
 
@@ -658,6 +730,19 @@ int Engine::compute_smoothness(double* out) {
 // (relaxation.hpp:225-244)
 // ---------------------------------------------------------------------------
 int Engine::step(int ma, double eta, double rho, const RelaxParams& cfg) {
+  int tn_split = 1;
+  if (gram_) {  // G = Q V - c, one product, one slab
+    tic(KC_GEMM_TN);
+    if (int rc = launch_gram(plan(p, p, ma, false, dTmapQ_ != nullptr), dV_, p, dG_, p, dAct_, dMa_))
+      return rc;
+    toc(KC_GEMM_TN, 2.0 * p * p * ma);
+  } else if (int rc = step_products(ma, tn_split)) {
+    return rc;
+  }
+  return step_prox(ma, eta, rho, cfg, tn_split);
+}
+
+int Engine::step_products(int ma, int& tn_split) {
   const GemmPlan p1 = plan(n, p, ma, false);
   tic(KC_GEMM_NN);
   if (ma >= oz_min_ && ozaki_enabled()) {  // tcgen05 kind::i8 emulated FP64 + l' epilogue
@@ -668,7 +753,7 @@ int Engine::step(int ma, double eta, double rho, const RelaxParams& cfg) {
   toc(KC_GEMM_NN, 2.0 * n * p * ma);
   const GemmPlan p2 = plan(p, n, ma, true);
   tic(KC_GEMM_TN);
-  int tn_split = p2.nsplit;
+  tn_split = p2.nsplit;
   if (ma >= oz_min_ && ozaki_enabled()) {  // tcgen05 kind::i8 emulated FP64 (ozaki.cuh)
     if (int rc = gemm_ozaki(true, false, dR_, n, dAct_, ma, dMa_, dG_, p, (long long)p * mcap_, &tn_split))
       return rc;
@@ -677,6 +762,10 @@ int Engine::step(int ma, double eta, double rho, const RelaxParams& cfg) {
     return rc;
   }
   toc(KC_GEMM_TN, 2.0 * n * p * ma);
+  return 0;
+}
+
+int Engine::step_prox(int ma, double eta, double rho, const RelaxParams& cfg, int tn_split) {
   cur_nsplit_ = tn_split;
   RelaxDev r{};
   r.p = p;
@@ -855,6 +944,24 @@ int Engine::run_pass(int m, const RelaxParams& cfg, double thr, double eta, doub
   a.bar = dBar_;
   const bool clus = resc_.on && m <= cluster_max_m_;
   a.res = clus ? resc_ : res_;
+  a.gram = gram_ ? 1 : 0;
+  if (gram_) {  // G = Q V - c (streaming 16-row tiles of Q, L2-resident)
+    GemmArgs& gq = a.gq;
+    gq = g1;
+    gq.M = p;
+    gq.K = p;
+    gq.A = dQ_;
+    gq.lda = p;
+    gq.B = dV_;
+    gq.ldb = p;
+    gq.C = dG_;
+    gq.ldc = p;
+    gq.ksplit = ((p + kBK - 1) / kBK) * kBK;
+    gq.y = dCq_;
+    gq.loss = kSquared;
+    gq.tmap = nullptr;
+    gq.probe = nullptr;
+  }
   a.big = ((n % 2) == 0 && (p % 2) == 0) ? big_min_ : 0;
   a.nn.tmap = res_.on ? nullptr : tmNN_;  // streaming mode's 128 x 64 tiles
   a.tn.tmap = res_.on ? nullptr : tmTN_;
@@ -904,7 +1011,9 @@ int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_
   // batches, X resident); when one iteration's X V + X'R is large (c4-sized
   // X), the standalone GEMM kernels (two CTAs per SM) run faster and launch
   // gaps no longer matter.
-  const double iter_flops = 4.0 * n * (double)p * m;
+  const double iter_flops = gram_ ? 2.0 * p * (double)p * m : 4.0 * n * (double)p * m;
+  if (gram_)
+    if ((rc = gram_prepare())) goto done;
   if (pass_grid_ > 0 && (res_.on || (m <= 2 * sms_ && iter_flops <= persist_max_flops_))) {
     // narrow batch: the whole relaxation as one persistent cooperative kernel
     if ((rc = run_pass(m, cfg, thr, eta, rho, dTrace, iter, n_evals, node_its))) goto done;

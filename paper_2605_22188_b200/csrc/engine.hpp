@@ -156,6 +156,8 @@ class Engine {
   int fail(int code, const std::string& msg);
   int cuda_fail(cudaError_t e, const char* what);
   int step(int ma, double eta, double rho, const RelaxParams& cfg);
+  int step_products(int ma, int& tn_split);
+  int step_prox(int ma, double eta, double rho, const RelaxParams& cfg, int tn_split);
   int run_pass(int m, const RelaxParams& cfg, double thr, double eta, double rho, double* dTrace,
                int& iter, int& n_evals, long long& node_its);
   int pass_grid_ = 0;       // CTAs of the persistent pass kernel (0: disabled)
@@ -196,7 +198,20 @@ class Engine {
     bool big = false;  // gemm_big.cuh tile (wide batches)
     dim3 grid;
   };
-  GemmPlan plan(int M, int K, int ncols, bool allow_split) const;
+  GemmPlan plan(int M, int K, int ncols, bool allow_split, bool allow_big = true) const;
+  // Squared loss with p <= n: the iteration gradient G = X'(X V - y) is
+  // formed as Q V - c with Q = X'X (p x p) and c = X'y computed once per
+  // engine (2 p^2 flops per column instead of 4 n p, one product instead of
+  // two).  The bound evaluations keep the X products (Psi from R = X B - y).
+  // BNBG_GRAM=0 disables.
+  bool gram_ = false;
+  double* dQ_ = nullptr;
+  double* dCq_ = nullptr;
+  int* dGramCnt_ = nullptr;  // device {p, 1}: column counts of the setup products
+  void* dTmapQ_ = nullptr;   // TMA descriptor of Q for the 128 x 64 tiles (p even, >= 132)
+  int gram_prepare();
+  int launch_gram(const GemmPlan& pl, const double* Bsrc, int ldb, double* C, int ldc,
+                  const int* act, const int* d_ncols);
   int launch_gemm(bool tn, int epi, const GemmPlan& pl, const double* Bsrc, int ldb, double* C,
                   int ldc, const int* act, const int* d_ncols, long long split_stride,
                   int part_ld);

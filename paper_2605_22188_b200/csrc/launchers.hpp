@@ -45,6 +45,8 @@ struct PassArgs {
   unsigned long long* prof;  // optional phase wall times (ns, CTA 0's view); nullptr: off
   unsigned* bar;             // grid barrier counter (zeroed before the launch)
   ResLayout res;
+  GemmArgs gq;  // gram: Q * V - c -> G (one slab), the iteration's only product
+  int gram;
   int big;                   // streaming mode: 128 x 64 register-tiled GEMM tiles when
                              // m_a >= big (gemm_big.cuh; needs n, p even); 0: never
 };

@@ -111,6 +111,26 @@ __device__ void pass_phase_nn(const PassArgs& a, const double* Bsrc, int ma, dou
   }
 }
 
+// Gram form of the iteration gradient (squared loss): G = Q V - c over
+// 16-row tiles of Q streamed from L2 (engine.hpp, gram_)
+static __device__ void pass_phase_gram(const PassArgs& a, int ma, double* smem, int* colmap,
+                                       const int* act) {
+  GemmArgs g = a.gq;
+  g.act = act;
+  const int fn = pass_fn(ma);
+  const int mt = (a.p + 15) / 16;
+  const int nt = (ma + 8 * fn - 1) / (8 * fn);
+  for (int t = blockIdx.x; t < mt * nt; t += gridDim.x) {
+    const int i = t % mt, j = t / mt;
+    if (fn == 1)
+      gemm_tile<false, 2, 1, EPI_DERIV, kPassNW>(g, ma, i, j, 0, smem, colmap);
+    else if (fn == 2)
+      gemm_tile<false, 2, 2, EPI_DERIV, kPassNW>(g, ma, i, j, 0, smem, colmap);
+    else
+      gemm_tile<false, 2, 4, EPI_DERIV, kPassNW>(g, ma, i, j, 0, smem, colmap);
+  }
+}
+
 // returns the split-K factor used (the consumers sum that many slabs)
 __device__ inline int pass_phase_tn(const PassArgs& a, int ma, double* smem, int* colmap,
                                     const int* act) {
@@ -543,14 +563,22 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
 
   while (iter < a.max_it && ma > 0) {  // relaxation.hpp:224-249
     ++iter;
-    phase_nn(r.V, false);
-    arrive(PH_NN);
-    grid_barrier(a.bar, bar_target, a.res.cluster);
-    mark(PH_NN);
-    nsplit = phase_tn();
-    arrive(PH_TN);
-    grid_barrier(a.bar, bar_target, a.res.cluster);
-    mark(PH_TN);
+    if (a.gram) {  // one product: G = Q V - c
+      pass_phase_gram(a, ma, smem, colmap, actp);
+      nsplit = 1;
+      arrive(PH_TN);
+      grid_barrier(a.bar, bar_target, a.res.cluster);
+      mark(PH_TN);
+    } else {
+      phase_nn(r.V, false);
+      arrive(PH_NN);
+      grid_barrier(a.bar, bar_target, a.res.cluster);
+      mark(PH_NN);
+      nsplit = phase_tn();
+      arrive(PH_TN);
+      grid_barrier(a.bar, bar_target, a.res.cluster);
+      mark(PH_TN);
+    }
     if (cached)
       cc.t = prox_column_impl<E, true>(r, nsplit, blockIdx.x, colsm, cc);
     else

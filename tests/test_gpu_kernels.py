@@ -336,3 +336,27 @@ def test_c1_certificate_same_with_and_without_cluster_pass(bnb, monkeypatch):
         assert c.status == "optimal" and c.support == [19, 39, 59, 79, 99]
         assert c.nodes_processed == 43
         assert abs(c.optimal_value - 6562.563358901953) <= 1e-9 * 6562.6
+
+
+@pytest.mark.parametrize("gram", ["1", "0"])
+@pytest.mark.parametrize("n,p,m,its", [(1000, 100, 12, 2000),   # persistent pass kernel
+                                       (200, 40, 300, 40),      # m > 2 x SMs: standalone kernels
+                                       (2000, 500, 70, 60)])    # 128 x 64 tiles of Q (p >= 132)
+def test_relax_gram_form_matches_oracle(bnb, orc, monkeypatch, gram, n, p, m, its):
+    """Squared loss, p <= n: the iteration gradient is Q V - c with Q = X'X,
+    c = X'y formed once (BNBG_GRAM=0: X'(X V - y) as the reference writes it,
+    relaxation.hpp:82-104).  Bounds, status, iteration counts and the iterates
+    match the oracle either way; the evaluations use X in both."""
+    monkeypatch.setenv("BNBG_GRAM", gram)
+    inst, eng = _engine(bnb, orc, n, p, 5, 0.7, 0, seed=13)
+    rng = np.random.default_rng(n + m)
+    st, kb = rnd_batch(rng, p, m, 5, all_free_first=True)
+    warm = np.zeros((p, m))
+    L = orc.smoothness(0, inst.X)
+    cfg = dict(smoothness=L, max_iterations=its)
+    res = eng.solve_batch_relaxation((st, kb, warm), bnb.RelaxConfig(**cfg), math.inf)
+    ob, obnd, ost, oit = orc.relax_batch(inst, st, kb, warm, math.inf, orc.relax_cfg(**cfg))
+    np.testing.assert_allclose(res.bounds, obnd, rtol=1e-6, atol=1e-6)
+    assert res.status.tolist() == ost.tolist()
+    assert res.iterations.tolist() == oit.tolist()
+    np.testing.assert_allclose(res.beta, ob, rtol=1e-6, atol=1e-7)
