@@ -200,12 +200,14 @@ int Engine::make_tmaps() {
 int Engine::fail(int code, const std::string& msg) {
   err = msg;
   defer_.clear();  // queued readbacks of the failed call are never copied out
+  pass_pending_ = false;
   return code;
 }
 
 int Engine::cuda_fail(cudaError_t e, const char* what) {
   err = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
   defer_.clear();
+  pass_pending_ = false;
   return 4;  // BNBG_CUDA_ERROR
 }
 
@@ -291,15 +293,34 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
       CK(pass_static_smem(colE_, &stat));
       const size_t limit = (size_t)optin - stat - 256;
       pass_smem_ = pass_smem(p, n2_, colE_);
-      // Gram iterations stream Q from L2; X is read at evaluations only
-      if (!(renv && renv[0] == '0') && !gram_) {
+      // small p (c1): Q, c and the column's B, V, states held in shared
+      // memory past the streaming region; every CTA iterates its column
+      // alone between evaluations (no grid barrier per iteration)
+      gram_local_off_ = 0;
+      const char* le = getenv("BNBG_GRAM_LOCAL");
+      const bool want_local =
+          gram_ && colE_ != 0 && !(le && le[0] == '0') && (size_t)p * p * 8 <= 128 * 1024;
+      const size_t gl_bytes = want_local ? gram_local_bytes(p) + 16 : 0;
+      // X residency: always tried without the Gram form; with it, only next to
+      // the local region (the evaluations read the resident X, the local
+      // iterations never touch it).  Streaming Gram iterations need the
+      // shared memory for their Q tiles.
+      if (!(renv && renv[0] == '0') && (!gram_ || want_local)) {
         ResLayout L;
-        const size_t rb = pass_res_plan(n, p, n2_, colE_, sms_, limit, &L);
+        const size_t rb = pass_res_plan(n, p, n2_, colE_, sms_, limit - gl_bytes, &L);
         if (L.on) {
           const char* cenv = getenv("BNBG_COLCACHE");
           if (cenv && cenv[0] == '0') L.off_cc = 0;  // diagnostics: no column cache
           res_ = L;
           pass_smem_ = rb;
+        }
+      }
+      if (want_local) {
+        const long long off = (long long)((pass_smem_ + 15) / 16 * 2);  // doubles, 16-byte aligned
+        const size_t bytes = 8 * (size_t)off + gram_local_bytes(p);
+        if (bytes <= limit) {
+          gram_local_off_ = off;
+          pass_smem_ = bytes;
         }
       }
       // one-cluster variant for small X (c1): 16 CTAs of one cluster hold X
@@ -309,7 +330,7 @@ int Engine::init(const double* X, const double* y, int n_, int p_, int loss_, in
       // sets the widest batch)
       resc_ = ResLayout{};
       const char* cenv = getenv("BNBG_CLUSTER_PASS");
-      if (res_.on && !(cenv && cenv[0] == '0')) {
+      if (res_.on && gram_local_off_ == 0 && !(cenv && cenv[0] == '0')) {
         constexpr int kCS = 16;
         ResLayout Lc;
         const size_t rbc = pass_res_plan(n, p, n2_, colE_, kCS, limit, &Lc, 4);
@@ -945,6 +966,8 @@ int Engine::run_pass(int m, const RelaxParams& cfg, double thr, double eta, doub
   const bool clus = resc_.on && m <= cluster_max_m_;
   a.res = clus ? resc_ : res_;
   a.gram = gram_ ? 1 : 0;
+  a.gram_local = gram_local_off_;
+  a.gram_c = dCq_;
   if (gram_) {  // G = Q V - c (streaming 16-row tiles of Q, L2-resident)
     GemmArgs& gq = a.gq;
     gq = g1;
@@ -975,15 +998,27 @@ int Engine::run_pass(int m, const RelaxParams& cfg, double thr, double eta, doub
   ++launches;
   CK(e);
   toc(KC_PASS, 0.0);  // end event right behind the kernel, before the readback sync
-  long long h_out[4] = {0, 0, 0, 0};
-  if (int rc = d2h_defer(h_out, dPassOut_, 3 * sizeof(long long))) return rc;
+  // the counters and the error word are read back with the pass's other
+  // results (relax_uploaded: one synchronisation); a traced pass needs its
+  // evaluation count first
+  if (int rc = d2h_defer(pass_out_h_, dPassOut_, 3 * sizeof(long long))) return rc;
   if (int rc = d2h(hPin_ + 1, dErr_, sizeof(int))) return rc;
-  if (int rc = sync_flush()) return rc;
-  iter = (int)h_out[0];
-  n_evals = (int)h_out[1];
-  node_its = h_out[2];
-  // algorithmic FP64 work: 4np per node-iteration (X V and X'R) -- evaluations excluded
-  kc_flops[KC_PASS] += 4.0 * n * p * (double)node_its;
+  pass_pending_ = true;
+  if (dTrace) {
+    if (int rc = sync_flush()) return rc;
+    return finish_pass(iter, n_evals, node_its);
+  }
+  return 0;
+}
+
+int Engine::finish_pass(int& iter, int& n_evals, long long& node_its) {
+  pass_pending_ = false;
+  iter = (int)pass_out_h_[0];
+  n_evals = (int)pass_out_h_[1];
+  node_its = pass_out_h_[2];
+  // FP64 work performed per node-iteration: X V and X'R (4np), or Q V (2p^2)
+  // in the Gram form -- evaluations excluded
+  kc_flops[KC_PASS] += (gram_ ? 2.0 * p * p : 4.0 * n * p) * (double)node_its;
   resolve_timing();
   if (hPin_[1] != 0x7fffffff)
     return fail(2, "relaxation: non-finite iterate in column " + std::to_string(hPin_[1]));
@@ -1038,8 +1073,6 @@ int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_
       ++n_evals;
     }
   }
-  out.iterations = iter;
-  out.node_iterations = node_its;
   if (read_beta) out.beta.resize((size_t)p * m);
   out.bounds.resize(m);
   out.status.resize(m);
@@ -1064,7 +1097,6 @@ int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_
   if (int rc_ = d2h_defer(out.bounds.data(), dBest_, sizeof(double) * m)) return rc_;
   if (int rc_ = d2h_defer(out.status.data(), dStatus_, sizeof(int) * m)) return rc_;
   if (int rc_ = d2h_defer(out.iters.data(), dIters_, sizeof(int) * m)) return rc_;
-  out.n_evals = n_evals;
   if (want_trace) {
     out.trace.resize((size_t)n_evals * m);
     for (int e = 0; e < n_evals; ++e)
@@ -1073,6 +1105,11 @@ int Engine::relax_uploaded(int m, const RelaxParams& cfg, double thr, bool want_
         return rc_;
   }
   if (int rc_ = sync_flush()) return rc_;
+  if (pass_pending_)
+    if ((rc = finish_pass(iter, n_evals, node_its))) goto done;
+  out.iterations = iter;
+  out.node_iterations = node_its;
+  out.n_evals = n_evals;
   resolve_timing();
 done:
   if (dTrace) dfree(dTrace);

@@ -160,6 +160,9 @@ class Engine {
   int step_prox(int ma, double eta, double rho, const RelaxParams& cfg, int tn_split);
   int run_pass(int m, const RelaxParams& cfg, double thr, double eta, double rho, double* dTrace,
                int& iter, int& n_evals, long long& node_its);
+  int finish_pass(int& iter, int& n_evals, long long& node_its);
+  long long pass_out_h_[4] = {0, 0, 0, 0};  // deferred readback of the pass counters
+  bool pass_pending_ = false;
   int pass_grid_ = 0;       // CTAs of the persistent pass kernel (0: disabled)
   size_t pass_smem_ = 0;
   long long* dPassOut_ = nullptr;
@@ -210,6 +213,7 @@ class Engine {
   int* dGramCnt_ = nullptr;  // device {p, 1}: column counts of the setup products
   void* dTmapQ_ = nullptr;   // TMA descriptor of Q for the 128 x 64 tiles (p even, >= 132)
   int gram_prepare();
+  long long gram_local_off_ = 0;  // pass kernel: double offset of the local-Gram region (0: off)
   int launch_gram(const GemmPlan& pl, const double* Bsrc, int ldb, double* C, int ldc,
                   const int* act, const int* d_ncols);
   int launch_gemm(bool tn, int epi, const GemmPlan& pl, const double* Bsrc, int ldb, double* C,

@@ -47,9 +47,18 @@ struct PassArgs {
   ResLayout res;
   GemmArgs gq;  // gram: Q * V - c -> G (one slab), the iteration's only product
   int gram;
+  long long gram_local;  // > 0: double offset of the local-Gram region (p <= 128): each
+                         // CTA iterates its own column between evaluations
+  const double* gram_c;  // c = X'y
   int big;                   // streaming mode: 128 x 64 register-tiled GEMM tiles when
                              // m_a >= big (gemm_big.cuh; needs n, p even); 0: never
 };
+
+// shared memory of the pass kernel's local-Gram region: Q (p x p), c, G, and
+// the column cache (B, V, states)
+inline size_t gram_local_bytes(int p) {
+  return 8 * ((size_t)p * p + 4 * (size_t)p) + (size_t)p + 64;
+}
 
 // ---- gemm_kernels.cu -------------------------------------------------------
 cudaError_t gemm_set_attrs();

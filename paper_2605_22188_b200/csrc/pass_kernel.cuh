@@ -464,7 +464,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
   // shared memory (ColCache), refreshed from global after every evaluation
   ColCache cc;
   bool cached = false;
-  const bool can_cache = res && E != 0 && a.res.off_cc > 0;
+  // local-Gram region (a.gram_local > 0): Q [p*p] c [p] G [p] | B [p] V [p] states [p]
+  double* gl = (E == 1 && a.gram_local > 0) ? smem + a.gram_local : nullptr;
+  const bool can_cache = (res && E != 0 && a.res.off_cc > 0) || (E != 0 && gl != nullptr);
   auto refresh = [&]() {
     ma = *(volatile int*)r.d_ma;
     for (int i = threadIdx.x; i < ma && i < kActCache; i += kPassThreads) s_act[i] = r.act[i];
@@ -478,7 +480,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
       cc.kb = r.kbar[b];
       cc.pf = r.pf[b];
       cc.t = r.t[b];
-      cc.B = smem + a.res.off_cc;
+      cc.B = gl ? gl + (size_t)p * p + 2 * p : smem + a.res.off_cc;
       cc.V = cc.B + p;
       uint8_t* stc = reinterpret_cast<uint8_t*>(cc.V + p);
       cc.st = stc;
@@ -490,6 +492,12 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
       __syncthreads();
     }
   };
+  if (gl) {  // Q and c, once per launch
+    const int p = r.p;
+    for (int e = threadIdx.x; e < p * p; e += kPassThreads) gl[e] = a.gq.A[e];
+    for (int j = threadIdx.x; j < p; j += kPassThreads) gl[(size_t)p * p + j] = a.gram_c[j];
+    __syncthreads();
+  }
   refresh();
   const bool prof = a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
   unsigned long long t_last = prof ? pass_clock() : 0ull;
@@ -562,8 +570,57 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
   };
 
   while (iter < a.max_it && ma > 0) {  // relaxation.hpp:224-249
+    if (E == 1 && gl && ma <= (int)gridDim.x) {  // p <= 128 implies E == 1
+      // local Gram iterations up to the next evaluation: the CTA owning a
+      // column forms G = Q V - c from shared memory (thread j: row j, k in
+      // order) and runs the prox on it; no other CTA is involved
+      const int nloc = min(a.check - iter % a.check, a.max_it - iter);
+      if (cached) {
+        const int p = r.p;
+        const double* Qs = gl;
+        const double* cs = gl + (size_t)p * p;
+        double* Gs = gl + (size_t)p * p + p;
+        RelaxDev rl = r;  // gsum(rl, 1, b, j) reads Gs[j]
+        rl.G = Gs - (size_t)cc.b * p;
+        rl.nsplit = 1;
+        rl.split_stride = 0;
+        for (int s2 = 0; s2 < nloc; ++s2) {
+          {
+            // p <= 128: thread t takes row t % 128 over the k half t / 128,
+            // two independent chains each; the halves and chains are added
+            // in a fixed order
+            const int j = threadIdx.x & 127, h = threadIdx.x >> 7;
+            const int kh = (p + 1) >> 1, kb = h * kh, ke = min(p, kb + kh);
+            double a0 = 0.0, a1 = 0.0;
+            if (j < p) {
+              int k2 = kb;
+              for (; k2 + 2 <= ke; k2 += 2) {
+                a0 += Qs[(size_t)k2 * p + j] * cc.V[k2];
+                a1 += Qs[(size_t)(k2 + 1) * p + j] * cc.V[k2 + 1];
+              }
+              if (k2 < ke) a0 += Qs[(size_t)k2 * p + j] * cc.V[k2];
+            }
+            if (h == 1 && j < p) Gs[j] = a0 + a1;  // upper half's partial
+            __syncthreads();
+            if (h == 0 && j < p) Gs[j] = ((a0 + a1) + Gs[j]) - cs[j];  // l' of the squared loss
+          }
+          __syncthreads();
+          cc.t = prox_column_impl<E, true>(rl, 1, blockIdx.x, colsm, cc);
+        }
+      }
+      iter += nloc;
+      node_its += (long long)ma * nloc;
+      arrive(PH_PROX);
+      grid_barrier(a.bar, bar_target, a.res.cluster);
+      mark(PH_PROX);
+      if (iter % a.check == 0) {
+        evaluate(iter);
+        last_eval = iter;
+      }
+      continue;
+    }
     ++iter;
-    if (a.gram) {  // one product: G = Q V - c
+    if (a.gram && !res) {  // one product: G = Q V - c (resident mode keeps the X form)
       pass_phase_gram(a, ma, smem, colmap, actp);
       nsplit = 1;
       arrive(PH_TN);

@@ -140,13 +140,23 @@ int Engine::branch_pool(int m, const int* slots, const double* lb_in, double pos
   CKL("k_branch_write");
   int tot[2];
   if (int rc_ = d2h_defer(tot, dTot_, sizeof(tot))) return rc_;
+  // small passes: every possible child record comes back with the counts
+  // (one synchronisation); large ones read the survivors' records only
+  const size_t ncmax = 2 * (size_t)m;
+  const bool whole = ncmax * (RI * sizeof(int) + sizeof(double)) <= (256u << 10);
+  if (whole) {
+    rec.resize(ncmax * RI);
+    rec_lb.resize(ncmax);
+    if (int rc_ = d2h_defer(rec.data(), dRec_, sizeof(int) * ncmax * RI)) return rc_;
+    if (int rc_ = d2h_defer(rec_lb.data(), dRecLb_, sizeof(double) * ncmax)) return rc_;
+  }
   if (int rc_ = sync_flush()) return rc_;
   survivors = tot[0];
   bad_column = tot[1];
   const size_t nc = 2 * (size_t)survivors;
   rec.resize(nc * RI);
   rec_lb.resize(nc);
-  if (nc) {
+  if (nc && !whole) {
     if (int rc_ = d2h_defer(rec.data(), dRec_, sizeof(int) * nc * RI)) return rc_;
     if (int rc_ = d2h_defer(rec_lb.data(), dRecLb_, sizeof(double) * nc)) return rc_;
     if (int rc_ = sync_flush()) return rc_;
