@@ -137,7 +137,7 @@ def _ncu_traffic(kernel_class, config):
         return None
     ent = d.get(f"{kernel_class}@{config}") or d.get(kernel_class, {})
     src = ent.get("source", "")
-    if f"_{config}." not in src and f"_{config}w." not in src:
+    if not any(f"_{config}{sep}" in src for sep in (".", "w.", "_")):
         return None
     return ent.get("dram_bytes_per_launch")
 
@@ -246,14 +246,17 @@ def cpu_baseline(config, time_limit):
             "lower_bound": c.lower_bound, "gap_percent": c.gap_percent}
 
 
-_EMULATED = ("; the iteration products of batches with >= 64 active columns run on the tcgen05 "
+_EMULATED = ("; the iteration products of batches with >= 16 active columns run on the tcgen05 "
              "kind::i8 tensor cores as an Ozaki-style FP64 emulation (36 int8 digit products "
              "per FP64 product, csrc/ozaki.cuh; the bound evaluation stays on DMMA), so "
              "'achieved' counts FP64-equivalent flops over the measured DMMA peak")
 ALGORITHMIC = {
     "gemm_xv": "2*n*p flops per active column per launch" + _EMULATED,
-    "gemm_xtr": "2*n*p flops per active column per launch" + _EMULATED,
-    "pass": "4*n*p flops per node-iteration (X*V and X'*R; bound evaluations not counted)",
+    "gemm_xtr": ("2*n*p flops per active column per launch" + _EMULATED + "; squared loss with "
+                 "p <= n: the iteration's only product is G = Q*V - c (Q = X'X), 2*p*p flops per "
+                 "active column on DMMA"),
+    "pass": "FP64 flops performed per node-iteration: 4*n*p (X*V and X'*R), or 2*p*p for the squared "
+            "loss with p <= n (G = Q*V - c, Q = X'X formed once per engine); bound evaluations not counted",
     "reopt": "4*q*n flops per support-iteration of the reference's projected gradient",
 }
 
