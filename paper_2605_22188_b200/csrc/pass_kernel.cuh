@@ -593,12 +593,26 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
             const int kh = (p + 1) >> 1, kb = h * kh, ke = min(p, kb + kh);
             double a0 = 0.0, a1 = 0.0;
             if (j < p) {
+              const double* qj = Qs + j;
               int k2 = kb;
-              for (; k2 + 2 <= ke; k2 += 2) {
-                a0 += Qs[(size_t)k2 * p + j] * cc.V[k2];
-                a1 += Qs[(size_t)(k2 + 1) * p + j] * cc.V[k2 + 1];
+              for (; k2 + 8 <= ke; k2 += 8) {  // 16 loads in flight, then the FMAs
+                double q[8], vv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                  q[u] = qj[(size_t)(k2 + u) * p];
+                  vv[u] = cc.V[k2 + u];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u += 2) {
+                  a0 += q[u] * vv[u];
+                  a1 += q[u + 1] * vv[u + 1];
+                }
               }
-              if (k2 < ke) a0 += Qs[(size_t)k2 * p + j] * cc.V[k2];
+              for (; k2 + 2 <= ke; k2 += 2) {
+                a0 += qj[(size_t)k2 * p] * cc.V[k2];
+                a1 += qj[(size_t)(k2 + 1) * p] * cc.V[k2 + 1];
+              }
+              if (k2 < ke) a0 += qj[(size_t)k2 * p] * cc.V[k2];
             }
             if (h == 1 && j < p) Gs[j] = a0 + a1;  // upper half's partial
             __syncthreads();
