@@ -87,6 +87,9 @@ int Engine::ensure_pool_batch(int m) {
   CK(cudaMallocAsync(&dFree_, sizeof(int) * 2 * (size_t)cap, stream_));
   CK(cudaMallocAsync(&dRec_, sizeof(int) * 2 * (size_t)cap * child_rec_ints(kk), stream_));
   CK(cudaMallocAsync(&dRecLb_, sizeof(double) * 2 * (size_t)cap, stream_));
+  // small passes read every record slot back (branch_pool): defined bytes
+  CK(cudaMemsetAsync(dRec_, 0xff, sizeof(int) * 2 * (size_t)cap * child_rec_ints(kk), stream_));
+  CK(cudaMemsetAsync(dRecLb_, 0, sizeof(double) * 2 * (size_t)cap, stream_));
   CK(cudaMallocAsync(&dOneLen_, sizeof(int) * cap, stream_));
   CK(cudaMallocAsync(&dOneIdx_, sizeof(int) * (size_t)cap * kk, stream_));
   pool_batch_cap_ = cap;

@@ -11,10 +11,14 @@ compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
   - re-opt kernels: cluster (st.async / mbarrier exchange), Gram (squared),
     shared-memory slices (large n);
   - packer, round/select, branch write, node pool, Rashomon;
-  - the NaN-key path of the prox (numeric_error) that memcheck flagged in r01.
+  - the NaN-key path of the prox (numeric_error) that memcheck flagged in r01;
+  - round-2 variants: squared loss with the Gram-form gradient (local
+    iterations for p <= 128, streaming Q tiles, the 128 x 64 tiles of Q with
+    its TMA descriptor), the X form (BNBG_GRAM=0), and the logistic pass
+    kernel as one 16-CTA cluster or as the 148-CTA grid.
 
 Usage: compute-sanitizer --tool memcheck python tools/sanitize_run.py [mode]
-mode: all (default) | resident | streaming | standalone | gemm | ozaki | reopt | errors
+mode: all (default) | resident | streaming | standalone | gemm | ozaki | reopt | errors | variants
 """
 import math
 import os
@@ -91,6 +95,28 @@ def errors():
         print("prox on NaN:", type(e).__name__, flush=True)
 
 
+def variants():
+    for env in ({"BNBG_GRAM_LOCAL": "0"}, {"BNBG_GRAM": "0"}, {"BNBG_CLUSTER_PASS": "0"}):
+        os.environ.update(env)
+        try:
+            print("variant", env, flush=True)
+            solves()
+        finally:
+            for v in env:
+                os.environ.pop(v)
+    i = inst(600, 300, 5, 0.5, 0)  # Gram product on 128 x 64 tiles of Q (p >= 132)
+    os.environ["BNBG_PERSISTENT"] = "0"
+    try:
+        with P.Engine(i) as eng:
+            nodes = [P.root_node(i.p(), i.k) for _ in range(70)]
+            for b, nd in enumerate(nodes):
+                nd.fixed_zero = [b % i.p()]
+            res = eng.solve_batch_relaxation(nodes, P.RelaxConfig(max_iterations=30))
+            print("gram wide batch", len(res.bounds), flush=True)
+    finally:
+        os.environ.pop("BNBG_PERSISTENT")
+
+
 def main():
     mode = sys.argv[1] if len(sys.argv) > 1 else "all"
     if mode in ("all", "resident"):
@@ -111,6 +137,8 @@ def main():
         reopt()
     if mode in ("all", "errors"):
         errors()
+    if mode in ("all", "variants"):
+        variants()
     print("sanitize_run done", flush=True)
 
 
