@@ -710,6 +710,33 @@ int Engine::compute_smoothness(double* out) {
   // the host synchronises once per batch instead of once per round; the
   // arithmetic is the oracle's sequential order (bit-identical L)
   double ps[4] = {0.0, 0.0, -1.0, 0.0};
+  // small p: one cooperative kernel loops the rounds on the device (every
+  // column of X'(X v) gets its own warp; no host synchronisation between
+  // rounds).  Larger p: the graph below (more columns in flight per round).
+  // BNBG_PW_COOP=0 forces the graph.
+  {
+    const char* ce = getenv("BNBG_PW_COOP");
+    int coop = 0, nb = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    if (coop && !(ce && ce[0] == '0') &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pw_all, 256, 0) == cudaSuccess &&
+        nb >= 1 && (p + 7) / 8 <= nb * sms_) {
+      const int G = std::max((p + 7) / 8, std::min(sms_, (n + 255) / 256));
+      int nn_ = n, pp_ = p;
+      const double* Xc = dX_;
+      void* args[] = {&nn_, &pp_, &Xc, &dv, &dxv, &dw, &dps};
+      ++launches;
+      CK(cudaLaunchCooperativeKernel((const void*)k_pw_all, dim3(G), dim3(256), args, 0, stream_));
+      if (int rc_ = d2h(ps, dps, sizeof(ps))) return rc_;
+      CK(cudaStreamSynchronize(stream_));
+      double result = ps[2];
+      if (result < 0.0) result = std::max(1.01 * c * ps[1], 1e-12);
+      *out = result;
+      return 0;
+    }
+    (void)cudaGetLastError();
+  }
   // 8 rounds (24 kernels) captured once as a CUDA graph and replayed: the
   // kernels of rounds past the stop or past round 100 return at once
   constexpr int kRounds = 8;

@@ -883,5 +883,129 @@ static __global__ void k_pw_step(int p, const double* w, double* v, double* ps) 
   }
 }
 
+// The whole power iteration as ONE cooperative kernel (small p: every column
+// of X'(X v) has its own warp in the grid): rounds loop on the device, the
+// three steps of a round (X v by rows, X'(X v) by columns, the sequential
+// v.w / |w| / stopping test on CTA 0) separated by grid barriers; the same
+// arithmetic and order as k_pw_xv / k_pw_xtv / k_pw_step, so L stays
+// bit-identical to the oracle's.  Values written by other CTAs are read
+// through L2 (__ldcg): L1 is not coherent across the grid.
+static __global__ void __launch_bounds__(256) k_pw_all(int n, int p, const double* __restrict__ X,
+                                                       double* v, double* xv, double* w,
+                                                       double* ps) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  constexpr int CH = 2048;
+  __shared__ double cv[CH], cw[CH];
+  __shared__ double prods[8][2][32];
+  __shared__ int s_dec;
+  __shared__ double s_wn;
+  const int G = gridDim.x, tid = threadIdx.x, wp = tid >> 5, lane = tid & 31;
+  for (;;) {
+    if (__ldcg(ps) != 0.0 || __ldcg(ps + 3) >= 100.0) break;  // losses.hpp:98-109
+    // X v: thread per row, j in order (k_pw_xv)
+    for (int i = blockIdx.x * 256 + tid; i < n; i += G * 256) {
+      constexpr int U = 16;
+      double bx[U], bv[U];
+      double s = 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        bx[u] = u < p ? __ldg(X + (size_t)u * n + i) : 0.0;
+        bv[u] = u < p ? __ldcg(v + u) : 0.0;
+      }
+      for (int j0 = 0; j0 < p; j0 += U) {
+        double nx[U], nv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = j0 + U + u;
+          nx[u] = j < p ? __ldg(X + (size_t)j * n + i) : 0.0;
+          nv[u] = j < p ? __ldcg(v + j) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j0 + u < p) s = __dadd_rn(s, __dmul_rn(bx[u], bv[u]));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          bx[u] = nx[u];
+          bv[u] = nv[u];
+        }
+      }
+      xv[i] = s;
+    }
+    grid.sync();
+    // X'(X v): warp per column, lane 0 adds the products in row order (k_pw_xtv)
+    for (int j = blockIdx.x * 8 + wp; j < p; j += G * 8) {
+      const double* col = X + (size_t)j * n;
+      double s = 0.0;
+      int buf = 0;
+      prods[wp][0][lane] = lane < n ? __dmul_rn(__ldg(col + lane), __ldcg(xv + lane)) : 0.0;
+      for (int i0 = 0; i0 < n; i0 += 32, buf ^= 1) {
+        const int in = i0 + 32 + lane;
+        const double nprod = in < n ? __dmul_rn(__ldg(col + in), __ldcg(xv + in)) : 0.0;
+        __syncwarp();
+        if (lane == 0) {
+          const double* pr = prods[wp][buf];
+          if (i0 + 32 <= n) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) s = __dadd_rn(s, pr[q]);
+          } else {
+            for (int q = 0; q < n - i0; ++q) s = __dadd_rn(s, pr[q]);
+          }
+        }
+        prods[wp][buf ^ 1][lane] = nprod;
+      }
+      if (lane == 0) w[j] = s;
+      __syncwarp();
+    }
+    grid.sync();
+    if (blockIdx.x == 0) {  // k_pw_step
+      double next = 0.0, nrm2 = 0.0;
+      for (int c0 = 0; c0 < p; c0 += CH) {
+        const int len = min(CH, p - c0);
+        for (int j = tid; j < len; j += 256) {
+          cv[j] = __ldcg(v + c0 + j);
+          cw[j] = __ldcg(w + c0 + j);
+        }
+        __syncthreads();
+        if (tid == 0)
+          for (int j = 0; j < len; ++j) next = __dadd_rn(next, __dmul_rn(cv[j], cw[j]));
+        __syncthreads();
+      }
+      for (int c0 = 0; c0 < p; c0 += CH) {
+        const int len = min(CH, p - c0);
+        for (int j = tid; j < len; j += 256) cw[j] = __ldcg(w + c0 + j);
+        __syncthreads();
+        if (tid == 0)
+          for (int j = 0; j < len; ++j) nrm2 = __dadd_rn(nrm2, __dmul_rn(cw[j], cw[j]));
+        __syncthreads();
+      }
+      if (tid == 0) {
+        const double wn = sqrt(nrm2);
+        int dec = 0;  // 0: continue, 1: zero / non-positive, 2: converged
+        if (wn == 0.0 || next <= 0.0)
+          dec = 1;
+        else if (ps[3] > 0.0 && fabs(next - ps[1]) <= 1e-4 * next)
+          dec = 2;
+        if (dec == 1)
+          ps[2] = 1e-12;
+        else
+          ps[1] = next;
+        s_dec = dec;
+        s_wn = wn;
+      }
+      __syncthreads();
+      const int dec = s_dec;
+      const double wn = s_wn;
+      if (dec != 1)
+        for (int j = tid; j < p; j += 256) v[j] = __ldcg(w + j) / wn;
+      __syncthreads();
+      if (tid == 0) {
+        if (dec != 0) ps[0] = 1.0;
+        ps[3] += 1.0;
+      }
+    }
+    grid.sync();
+  }
+}
 
 }  // namespace bnbg
