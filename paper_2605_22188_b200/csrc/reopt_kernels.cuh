@@ -895,9 +895,10 @@ static __global__ void __launch_bounds__(256) k_pw_all(int n, int p, const doubl
                                                        double* ps) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  constexpr int CH = 2048;
+  constexpr int CH = 1024;
   __shared__ double cv[CH], cw[CH];
-  __shared__ double prods[8][2][32];
+  constexpr int CW = 128;  // products per chain step: 4 loads per lane in flight
+  __shared__ double prods[8][2][CW];
   __shared__ int s_dec;
   __shared__ double s_wn;
   const int G = gridDim.x, tid = threadIdx.x, wp = tid >> 5, lane = tid & 31;
@@ -938,21 +939,31 @@ static __global__ void __launch_bounds__(256) k_pw_all(int n, int p, const doubl
       const double* col = X + (size_t)j * n;
       double s = 0.0;
       int buf = 0;
-      prods[wp][0][lane] = lane < n ? __dmul_rn(__ldg(col + lane), __ldcg(xv + lane)) : 0.0;
-      for (int i0 = 0; i0 < n; i0 += 32, buf ^= 1) {
-        const int in = i0 + 32 + lane;
-        const double nprod = in < n ? __dmul_rn(__ldg(col + in), __ldcg(xv + in)) : 0.0;
+#pragma unroll
+      for (int d = 0; d < CW / 32; ++d) {
+        const int i = lane + 32 * d;
+        prods[wp][0][i] = i < n ? __dmul_rn(__ldg(col + i), __ldcg(xv + i)) : 0.0;
+      }
+      for (int i0 = 0; i0 < n; i0 += CW, buf ^= 1) {
+        double np[CW / 32];  // the next step's products, loaded during this chain
+#pragma unroll
+        for (int d = 0; d < CW / 32; ++d) {
+          const int in = i0 + CW + lane + 32 * d;
+          np[d] = in < n ? __dmul_rn(__ldg(col + in), __ldcg(xv + in)) : 0.0;
+        }
         __syncwarp();
         if (lane == 0) {
           const double* pr = prods[wp][buf];
-          if (i0 + 32 <= n) {
+          if (i0 + CW <= n) {
 #pragma unroll
-            for (int q = 0; q < 32; ++q) s = __dadd_rn(s, pr[q]);
+            for (int q = 0; q < CW; ++q) s = __dadd_rn(s, pr[q]);
           } else {
             for (int q = 0; q < n - i0; ++q) s = __dadd_rn(s, pr[q]);
           }
         }
-        prods[wp][buf ^ 1][lane] = nprod;
+        __syncwarp();
+#pragma unroll
+        for (int d = 0; d < CW / 32; ++d) prods[wp][buf ^ 1][lane + 32 * d] = np[d];
       }
       if (lane == 0) w[j] = s;
       __syncwarp();
